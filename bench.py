@@ -1,0 +1,407 @@
+"""Benchmark of the B200-native featlsq hot path (BASELINE.json metric:
+"RRQR filter+precond sec & GFLOP/s; LSQR matvec GB/s vs HBM roofline; solve
+sec").
+
+One step = one full solve of the workload: K1 assembly -> K2 truncated RRQR
+(filter + preconditioner factors) -> K4 device LSQR with a fixed budget of
+--lsqr-iters iterations (the reference has no stopping rule) -> K5 recovery.
+Default workload: cfg4, the north-star 2D 32x32-subdomain Helmholtz system
+(643 200 x 524 288, M = 512), synthetic inputs per SURVEY.md §8(d).
+
+`value` (solves/s, whole job) is timed with CUDA events on the launching
+stream with the inputs already in HBM; `e2e` is the same metric through the
+public Python API (`assemble` / `filter_system` / `precondition` / `lsqr` /
+`recover_solution`) with host inputs and host outputs, copies included.
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port in oracle/featlsq_oracle.py: scipy LAPACK dgeqp3/dorgqr + CSR
+SpMV, as the reference does) on a bounded sample of the same workload and
+extrapolates per block / per nonzero to the full solve.
+
+Multi-GPU: replicas (each rank solves its own seed of the workload; the
+north star pins one GPU per solve), timed as the
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RRQR filter+precond sec & GFLOP/s; LSQR matvec GB/s vs HBM roofline; solve sec"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--lsqr-iters", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-blocks", type=int, default=8)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        loaded = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def fp64_peak(torch, D, _lib):
+    """Measured FP64 peak (TFLOP/s): DFMA and DMMA probes, best of 3."""
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    res = {}
+    grid, iters = 148 * 8, 4096
+    for mode, name in ((0, "dfma"), (1, "dmma")):
+        best = 0.0
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.check(_lib.lib().fl_probe_fp64(mode, grid, iters, D.ptr(out), D.stream_ptr()),
+                       "probe")
+            e1.record()
+            torch.cuda.synchronize()
+            flops = grid * 256 * iters * 16 if mode == 0 else grid * 8 * iters * 4 * 512
+            best = max(best, flops / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        res[name] = round(best, 2)
+    return res
+
+
+# ---------------------------------------------------------------- work counts
+def rrqr_flops(m, K, r):
+    """F_alg (truncated QRCP + thin Q + initial norms) and
+    F_ref (full dgeqp3 + dorgqr, what the reference executes)."""
+    m, r = m.astype(np.float64), r.astype(np.float64)
+    f_alg = (4 * m * K * r - 2 * (m + K) * r ** 2 + (4 / 3) * r ** 3
+             + 2 * m * r ** 2 - (2 / 3) * r ** 3 + 2 * m * K)
+    kk = np.minimum(m, K)
+    f_ref = 4 * m * K * kk - (4 / 3) * kk ** 3
+    return float(f_alg.sum()), float(f_ref.sum())
+
+
+# ---------------------------------------------------------------- product arm
+def product(args, rank, world, local_rank):
+    import torch
+    import paper_2506_17626_b200 as fl
+    from paper_2506_17626_b200 import _device as D, _lib, workloads
+    from paper_2506_17626_b200.assembly import AssemblyPlan
+    from paper_2506_17626_b200.filtering import recover_solution_device
+    from paper_2506_17626_b200.solvers import DeviceLsqr
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    wl = workloads.build(args.config, seed=rank)
+    iters = args.lsqr_iters
+
+    # ---- device-resident pipeline: host preparation outside the timed region
+    plan = AssemblyPlan(wl.problem, wl.dec, wl.basis, wl.interior_per_dim)
+    rhs_dev = D.to_dev(plan.rhs)
+    store = plan.new_store()
+    system = plan.system(store)
+    state = {}
+
+    def step(ev):
+        ev[0].record()
+        plan.launch(store)
+        ev[1].record()
+        fs = fl.filter_system(system, wl.sigma)
+        ev[2].record()
+        op = fl.precondition(fs)
+        run = state.get("run")
+        if run is None or run.blocks is not op.device_blocks:
+            run = DeviceLsqr(op.device_blocks, iters)
+        state["run"] = run
+        run.reset_state(1, track_best=True)
+        run.init(rhs_dev)
+        ev[3].record()
+        run.iterate(1, iters)
+        ev[4].record()
+        coeffs, _ = recover_solution_device(fs, run.x)
+        ev[5].record()
+        state["fs"] = fs
+        return coeffs
+
+    def events():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+
+    for _ in range(args.warmup):
+        step(events())
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [events() for _ in range(args.steps)]
+    t_start.record()
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    if dist:
+        tt = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+        dist.barrier()
+
+    def avg(a, b):
+        return float(np.mean([e[a].elapsed_time(e[b]) for e in evs])) / 1e3
+
+    t_asm, t_rrqr, t_init, t_lsqr, t_rec = avg(0, 1), avg(1, 2), avg(2, 3), avg(3, 4), avg(4, 5)
+    fs = state["fs"]
+    L = fs.qstore.layout
+    m = L.m.astype(np.int64)
+    nnz_q = int(np.sum(m * fs.ranks))
+    nnz_a = int(m.sum()) * L.K
+    f_alg, f_ref = rrqr_flops(m, L.K, fs.ranks)
+    bytes_it = 8.0 * (2 * nnz_q + 2 * L.nrows + 6 * fs.kept_total)
+    t_it = t_lsqr / iters
+    hbm, hbm_src = peaks()
+    fp64 = fp64_peak(torch, D, _lib)
+    fp64_peak_tf = max(fp64.values())
+    st = state["run"].read_state()
+    stage_t = {"assemble": t_asm, "rrqr": t_rrqr, "lsqr": t_lsqr + t_init, "recover": t_rec}
+    dominant = max(stage_t, key=stage_t.get)
+    step_s = elapsed / args.steps
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.config, {}).get("lsqr_bytes_per_iter")
+    out = {
+        "metric": METRIC, "value": round(world / step_s, 6), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md §8(d) inputs, seeded)",
+        "config": {"workload": f"{args.config}: {wl.description}",
+                   "lsqr_iters_per_solve": iters, "sigma": wl.sigma,
+                   "rows": L.nrows, "cols": int(L.J * L.K), "kept": int(fs.kept_total),
+                   "l2": f"inputs larger than L2 (Q {nnz_q * 8 / 1e9:.2f} GB, A {nnz_a * 8 / 1e9:.2f} GB)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "kernel": "LSQR iteration (qv + ured + qtu)",
+                     "achieved": round(bytes_it / t_it / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(bytes_it / t_it / 1e9 / hbm, 4),
+                     "traffic": traffic, "peak_source": hbm_src,
+                     "algorithmic_bytes_per_launch": bytes_it, "dominant_stage": dominant},
+        "stages": {
+            "assemble": {"ms": round(t_asm * 1e3, 3), "GB/s": round(8 * nnz_a / t_asm / 1e9, 1),
+                         "frac_hbm": round(8 * nnz_a / t_asm / 1e9 / hbm, 4)},
+            "rrqr_filter_precond": {"ms": round(t_rrqr * 1e3, 3),
+                                    "GFLOP/s_alg": round(f_alg / t_rrqr / 1e9, 1),
+                                    "GFLOP/s_ref": round(f_ref / t_rrqr / 1e9, 1),
+                                    "F_alg_TF": round(f_alg / 1e12, 4),
+                                    "frac_fp64_peak": round(f_alg / t_rrqr / 1e12 / fp64_peak_tf, 4),
+                                    "fp64_peak_TF_measured": fp64},
+            "lsqr": {"ms_per_iter": round(t_it * 1e3, 4), "GB/s": round(bytes_it / t_it / 1e9, 1),
+                     "frac_hbm": round(bytes_it / t_it / 1e9 / hbm, 4), "init_ms": round(t_init * 1e3, 3),
+                     "phibar": st.phibar, "iterations": int(st.it)},
+            "recover": {"ms": round(t_rec * 1e3, 3)},
+            "solve_s": round(step_s, 4),
+        },
+        "clocks": clk,
+        "gpu_launches": args.steps * (1 + 1 + 2 + 3 * iters + 1),
+    }
+
+    # ---- end to end through the public API, host buffers
+    if not args.no_e2e:
+        fl_steps = max(args.e2e_steps, 1)
+
+        def e2e_step():
+            system_h = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+            fs_h = fl.filter_system(system_h, wl.sigma)
+            res = fl.lsqr(fl.precondition(fs_h), system_h.rhs, iters)
+            return fl.recover_solution(fs_h, res.solution)
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        x0 = dict(D.XFER)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(fl_steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        t_e2e = e0.elapsed_time(e1) / 1e3
+        if dist:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        out["e2e"] = {"value": round(world * fl_steps / t_e2e, 6), "unit": UNIT,
+                      "h2d_bytes_per_step": int((D.XFER["h2d"] - x0["h2d"]) / fl_steps),
+                      "d2h_bytes_per_step": int((D.XFER["d2h"] - x0["d2h"]) / fl_steps),
+                      "ms_per_step": round(t_e2e / fl_steps * 1e3, 2)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_sample(wl, iters, args.cpu_blocks, n_samples=1)
+    return out
+
+
+# ---------------------------------------------------------------- CPU (reference algorithm)
+def cpu_sample(wl, iters, nblk, n_samples=1):
+    """Bounded sample of the reference algorithm on the host (oracle port:
+    the reference's own numpy/scipy path). Times assembly + filtering
+    (scipy dgeqp3/dorgqr, BLAS threads = all cores) + recovery of `nblk`
+    evenly spread blocks and 5 CSR LSQR iterations over their Q blocks,
+    then extrapolates per block and per Q nonzero to the full solve."""
+    from oracle import featlsq_oracle as O
+    J = wl.dec.subdomain_count
+    sel = np.linspace(0, J - 1, nblk).round().astype(int).tolist()
+    best = None
+    for _ in range(n_samples):
+        t0 = time.perf_counter()
+        sysd = O.assemble(wl.problem, wl.dec, wl.basis, wl.interior_per_dim, only=sel)
+        t1 = time.perf_counter()
+        fb, off = O.filter_system(sysd, wl.sigma)
+        t2 = time.perf_counter()
+        q = O.q_operator(fb, off, sysd["row_count"])
+        rhs = sysd["rhs"]
+        t3 = time.perf_counter()
+        O.lsqr(lambda v: q @ v, lambda r: q.T @ r, q.shape[1], rhs, 5)
+        t4 = time.perf_counter()
+        O.recover_solution(fb, off, np.ones(int(off[-1])), sysd["column_count"])
+        t5 = time.perf_counter()
+        nnz_s = sum(b["q"].size for b in fb)
+        scale_blk = J / len(sel)
+        t_it = (t4 - t3) / 5 * scale_blk           # per-nonzero extrapolation
+        solve = scale_blk * ((t1 - t0) + (t2 - t1) + (t5 - t4)) + iters * t_it
+        rec = dict(solve_s=solve, assemble_s=scale_blk * (t1 - t0),
+                   rrqr_s=scale_blk * (t2 - t1), lsqr_ms_per_iter=t_it * 1e3,
+                   recover_s=scale_blk * (t5 - t4), nnz_q_sample=int(nnz_s),
+                   sample_s=t5 - t0)
+        if best is None or rec["solve_s"] < best["solve_s"]:
+            best = rec
+    return {"value": round(1.0 / best["solve_s"], 8), "unit": UNIT, "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": (f"{len(sel)} of {J} blocks (assembly + scipy dgeqp3/dorgqr RRQR + "
+                       f"recovery) and 5 CSR LSQR iterations over their Q blocks, extrapolated "
+                       f"per block / per Q nonzero to the full {iters}-iteration solve; "
+                       f"BLAS threads = {os.cpu_count()}, CSR SpMV single-threaded; "
+                       f"host {platform.processor() or platform.machine()}"),
+            "stages": {k: round(v, 4) if isinstance(v, float) else v for k, v in best.items()}}
+
+
+def reference(args, rank, world):
+    from paper_2506_17626_b200 import workloads
+    wl = workloads.build(args.config, seed=0)
+    iters = args.lsqr_iters
+    if args.warmup > 0:  # first scipy.linalg.qr call pays LAPACK start-up
+        cpu_sample(wl, iters, max(2, args.cpu_blocks // 4))
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_sample(wl, iters, args.cpu_blocks))
+    wall = time.perf_counter() - t0
+    best = max(vals, key=lambda v: v["value"])
+    return {"impl": "reference", "metric": METRIC, "value": best["value"], "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 / best["value"], 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8(d) inputs, seeded)",
+            "config": {"workload": f"{args.config}: {wl.description}",
+                       "lsqr_iters_per_solve": iters, "sigma": wl.sigma},
+            "cpu_baseline": {"value": best["value"], "unit": UNIT, "cores": best["cores"],
+                             "kind": best["kind"], "sample": best["sample"]},
+            "e2e": {"value": best["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "stages": best["stages"], "wall_s": round(wall, 2)}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(reference(args, rank, world)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    out = product(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

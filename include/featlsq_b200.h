@@ -1,0 +1,202 @@
+/*
+ * featlsq_b200.h — C-ABI of the B200-native RRQR-filtered ELM-FBPINN
+ * least-squares hot path (arXiv 2506.17626, reference package `featlsq`).
+ *
+ * Plain C: device pointers, int32/int64 sizes, an opaque CUDA stream handle
+ * (`void*`, a cudaStream_t; NULL = legacy default stream). No allocation of
+ * caller-visible memory happens inside the library; every call is stream
+ * ordered and reentrant (no global mutable state). Return value 0 = OK,
+ * negative = one of FL_ERR_* below, mapped 1:1 by the host layer onto the
+ * reference exceptions (`featlsq/errors.py:4-41`).
+ *
+ * Entry point -> reference interface it replaces (reference tree
+ * pkg/src/featlsq/):
+ *   fl_assemble            assembly.py:124-238 `assemble` per-block loop
+ *                          (+ domains.py:109-173 window jets, basis.py:106-133
+ *                          feature jets, assembly.py:107-114, problems.py:39-47)
+ *   fl_rrqr                filtering.py:92-115 `filter_system` ->
+ *                          linalg.py:58-97 `qr_column_pivot` (dgeqp3+dorgqr)
+ *   fl_blockop_apply       filtering.py:146-150 PreconditionedOperator.apply,
+ *                          assembly.py:91-96 `apply`
+ *   fl_blockop_apply_t     filtering.py:152-157 apply_transpose,
+ *                          assembly.py:99-104 `apply_transpose`
+ *   fl_lsqr_*              solvers.py:87-145 `lsqr` (device-resident loop)
+ *   fl_backsub_scatter     filtering.py:169-183 `recover_solution` ->
+ *                          linalg.py:100-112 `back_substitute` (dtrtrs)
+ */
+#ifndef FEATLSQ_B200_H
+#define FEATLSQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes */
+#define FL_OK                    0
+#define FL_ERR_INVALID         (-1)  /* InvalidInputError */
+#define FL_ERR_DEGENERATE      (-2)  /* DegenerateSubdomainError (see fl_rrqr out-param) */
+#define FL_ERR_DIVERGENCE      (-3)  /* DivergenceError (see fl_lsqr_state.diverged_at) */
+#define FL_ERR_SINGULAR        (-4)  /* SingularFactorError */
+#define FL_ERR_CUDA            (-5)  /* launch / runtime failure */
+
+/* activations (basis.py:36-40) */
+#define FL_ACT_TANH    0
+#define FL_ACT_SIN     1
+#define FL_ACT_SIGMOID 2
+
+/* ------------------------------------------------------------------------
+ * Block store: J per-subdomain dense blocks, each column-major with leading
+ * dimension ld[j] (multiple of 16 doubles, zero padded), concatenated at
+ * element offsets off[j]. Block j has m[j] rows (global ids rows[row_off[j]
+ * .. row_off[j]+m[j])) and ncols[j] columns mapped to the y-space entries
+ * col_off[j] .. col_off[j]+ncols[j]. The same layout carries the raw blocks
+ * A_j (ncols = K, col_off = j*K) and the orthonormal blocks Q_j (ncols = r_j,
+ * col_off = prefix sums of r_j). `gptr/gsrc` is the row-gather map: for
+ * global row g, gsrc[gptr[g]..gptr[g+1]) are the partial-buffer positions
+ * (row_off[j] + local row) of the blocks covering g, in increasing j.
+ * ---------------------------------------------------------------------- */
+typedef struct fl_blockop {
+  int32_t nblocks;          /* J */
+  int32_t nrows;            /* global row count N */
+  int64_t ncols_total;      /* y-space length */
+  int64_t partial_len;      /* sum_j m[j] */
+  int32_t max_rows;         /* max_j m[j]     (shared-memory sizing) */
+  int32_t max_ncols;        /* max_j ncols[j] (shared-memory sizing) */
+  const double* vals;       /* block values */
+  const int64_t* off;       /* (J,) element offsets */
+  const int32_t* ld;        /* (J,) */
+  const int32_t* m;         /* (J,) */
+  const int32_t* ncols;     /* (J,) */
+  const int64_t* col_off;   /* (J,) */
+  const int64_t* row_off;   /* (J,) */
+  const int32_t* rows;      /* (partial_len,) global row of each block row */
+  const int32_t* gptr;      /* (N+1,) */
+  const int32_t* gsrc;      /* (partial_len,) */
+  /* launch tables (host-built, device-resident) */
+  int32_t n_row_tiles;      /* tiles of FL_ROW_TILE rows */
+  const int32_t* row_tiles; /* (n_row_tiles, 2): block, first row */
+  int32_t n_col_tiles;      /* tiles of FL_COL_TILE columns */
+  const int32_t* col_tiles; /* (n_col_tiles, 2): block, first column */
+  double* partial;          /* (partial_len,) scratch */
+  double* red_scratch;      /* (>= max(n_row_tiles, n_col_tiles) + 64) scratch */
+  unsigned int* counter;    /* (4,) zero-initialised scratch */
+} fl_blockop;
+
+#define FL_ROW_TILE 256
+#define FL_COL_TILE 32
+
+/* ------------------------------------------------------------------------
+ * Assembly (assembly.py:124-238). Row r of block j: r < prod(box_cnt) is the
+ * interior lattice point with per-dim index box_lo[i] + (C-order digit i of
+ * r); otherwise constraint entry con_idx[con_ptr[j] + r - box] (a point index
+ * into con_pts) of group con_grp[...]. All pointers are device pointers.
+ * ---------------------------------------------------------------------- */
+typedef struct fl_assembly_desc {
+  int32_t dim;              /* d <= 3 */
+  int32_t nsub;             /* J */
+  int32_t count_per_dim;    /* S */
+  int32_t nfeat;            /* K */
+  int32_t activation;       /* FL_ACT_* */
+  int32_t ngroups;          /* constraint groups (<= 7) */
+  int32_t reach;            /* ceil(overlap_ratio): centers within +-reach of
+                               the own center can cover a point of block j */
+  const double* centers;    /* (d, S) decomposition centers */
+  const double* half;       /* (d,) half widths */
+  const double* weights;    /* (J, K, d) first-layer weights */
+  const double* biases;     /* (J, K) first-layer biases */
+  const double* axes;       /* concatenated lattice axes */
+  const int64_t* axis_off;  /* (d,) start of axis i in `axes` */
+  const double* op_coef;    /* (1+G, 2+2d): value, weight, first[d], second[d]
+                               row 0 = interior operator, 1+g = group g */
+  const double* con_pts;    /* (Ncp, d) constraint points */
+  const int32_t* box;       /* (J, d, 2): lo, count */
+  const int64_t* con_ptr;   /* (J+1,) */
+  const int32_t* con_idx;   /* constraint point index */
+  const int32_t* con_grp;   /* constraint group */
+  int32_t n_tiles;          /* row tiles of FL_ASM_TILE rows */
+  const int32_t* tiles;     /* (n_tiles, 2): block, first row */
+} fl_assembly_desc;
+
+#define FL_ASM_TILE 64
+
+int fl_assemble(const fl_assembly_desc* desc, const fl_blockop* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Truncated column-pivoted Householder QR of every block, in place
+ * (linalg.py:58-97 rule: LAPACK dgeqp3 pivot choice, stop at the first
+ * |R_tt| < sigma |R_00|, sigma = 0 keeps min(m, K)). On return block j's
+ * first rank[j] columns hold Q_j (thin, sign-normalised so diag R > 0),
+ * R[j*K*K ..] holds R_j column-major with leading dimension K, perm[j*K ..]
+ * the pivot order (perm[j*K + t] = original local column of pivot t),
+ * diag[j*K + t] = |R_tt| / |R_00|. rank[j] = -1 flags a non-finite block.
+ * max_rows bounds m[j] over all blocks.
+ * ---------------------------------------------------------------------- */
+int fl_rrqr(const fl_blockop* blocks, int32_t K, int32_t max_rows, double sigma, double* R,
+            int32_t* perm, int32_t* rank, double* diag, void* stream);
+
+/* y-space -> rows: out[g] = sum over covering blocks of (B_j x_j)[g] */
+int fl_blockop_apply(const fl_blockop* op, const double* x, double* out, void* stream);
+/* rows -> y-space: out_j = B_j^T r[I_j] */
+int fl_blockop_apply_t(const fl_blockop* op, const double* r, double* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Device LSQR (solvers.py:87-145). State lives in device memory; the host
+ * reads only fl_lsqr_state after the loop.
+ * ---------------------------------------------------------------------- */
+typedef struct fl_lsqr_state {
+  double alpha, beta, rhobar, phibar, rho, c, s, phi, theta;
+  double beta_prev;         /* scale of the stored (unnormalised) u */
+  double best;              /* monitor best residual */
+  /* scipy stopping-rule accumulators (scipy.sparse.linalg.lsqr) */
+  double anorm, ddnorm, xxnorm, z, cs2, sn2, bnorm, atol, btol, ctol;
+  int64_t it;               /* iterations completed */
+  int64_t best_it;          /* monitor best iteration (-1 none) */
+  int64_t diverged_at;      /* first non-finite iteration, 0 = none */
+  int32_t done;             /* 1 = loop finished (breakdown / rule / divergence) */
+  int32_t breakdown;
+  int32_t istop;            /* scipy rule code when a tolerance stopped it */
+  int32_t use_rule;
+  int32_t stride;           /* monitor stride */
+  int32_t nonfinite;        /* scratch flag set by any CTA seeing a non-finite x */
+} fl_lsqr_state;
+
+typedef struct fl_lsqr_vecs {
+  double* u;                /* (N,) unnormalised u; true u = u / beta_prev */
+  double* v;                /* (n,) */
+  double* vp;               /* (n,) unnormalised v' */
+  double* w;                /* (n,) */
+  double* x;                /* (n,) */
+  double* xbest;            /* (n,) monitor best iterate */
+  double* trace;            /* (max_iters+1,) phibar per iteration */
+} fl_lsqr_vecs;
+
+/* rhs -> u, beta, v = Q^T u / alpha, w = v (solvers.py:98-117) */
+int fl_lsqr_init(const fl_blockop* op, const double* rhs, fl_lsqr_vecs* vecs,
+                 fl_lsqr_state* st, void* stream);
+/* iterations first_it .. first_it+count-1 (solvers.py:119-144); every
+ * kernel is a no-op once st->done is set, so a caller may enqueue the whole
+ * budget (or capture it in a CUDA graph) without host synchronisation. */
+int fl_lsqr_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st,
+                    int64_t first_it, int64_t count, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Recovery (filtering.py:169-183): coeffs[kept global column] = R_j^{-1} y_j,
+ * every other entry of coeffs (length J*K) exactly 0.
+ * ---------------------------------------------------------------------- */
+int fl_backsub_scatter(int32_t nblocks, int32_t K, const double* R, const int32_t* rank,
+                       const int32_t* perm, const int64_t* y_off, const double* y,
+                       double* coeffs, int32_t* singular_block, void* stream);
+
+/* diagnostics: FP64 throughput probe (mode 0 DFMA, 1 DMMA m8n8k4); flops
+ * per call = grid*256*iters*16 (mode 0) or grid*8*iters*2048 (mode 1) */
+int fl_probe_fp64(int32_t mode, int32_t grid, int32_t iters, double* out, void* stream);
+
+/* build metadata */
+const char* fl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEATLSQ_B200_H */

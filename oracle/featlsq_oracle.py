@@ -158,9 +158,10 @@ def lattice_axes(problem, dec, basis, interior_per_dim):
     return counts, axes
 
 
-def assemble(problem, dec, basis, interior_per_dim):
+def assemble(problem, dec, basis, interior_per_dim, only=None):
     """Returns dict(blocks=[(rows int64, matrix (m, K))], rhs, row_count,
-    column_count, interior_count, axes)."""
+    column_count, interior_count, axes). `only` restricts the per-block loop
+    to the listed subdomains (bounded CPU-baseline samples)."""
     d = dec.dim
     counts, axes = lattice_axes(problem, dec, basis, interior_per_dim)
     mesh = np.meshgrid(*axes, indexing="ij")
@@ -177,9 +178,9 @@ def assemble(problem, dec, basis, interior_per_dim):
         off += n_con
     k = basis.feature_count
     blocks = []
-    for j in range(dec.subdomain_count):
+    for j in (range(dec.subdomain_count) if only is None else only):
         idx = np.unravel_index(j, (dec.count_per_dim,) * d)
-        dim_idx = [np.nonzero(np.abs(axes[i] - dec.centers[i, idx[i]]) < dec.half_widths[i])[0]
+        dim_idx =[np.nonzero(np.abs(axes[i] - dec.centers[i, idx[i]]) < dec.half_widths[i])[0]
                    for i in range(d)]
         row_sets, parts = [], []
         if all(ix.size for ix in dim_idx):

@@ -1,0 +1,30 @@
+"""B200-native (sm_100a) drop-in for the featlsq hot path (arXiv 2506.17626):
+assemble -> filter_system (truncated RRQR) -> precondition -> lsqr ->
+recover_solution, with the same names, signatures and object surface as the
+reference stage API (featlsq assembly.py:124, filtering.py:92/165/169,
+solvers.py:87). Kernels: csrc/*.cu, C-ABI: include/featlsq_b200.h.
+"""
+
+from .assembly import GlobalSystem, SubdomainBlock, apply, apply_transpose, assemble
+from .basis import ACTIVATIONS, FeatureBasis, init_basis
+from .domains import Decomposition, Domain, decompose
+from .errors import (CapExceededError, CoverageError, DegenerateSubdomainError, DeviceError,
+                     DivergenceError, InvalidInputError, SingularFactorError)
+from .filtering import (FilteredBlock, FilteredSystem, PreconditionedOperator, filter_system,
+                        precondition, recover_solution)
+from .linalg import PivotedQR, RandomSource, back_substitute, lattice_counts, qr_column_pivot
+from .problems import ConstraintRows, LinearOperator2, ProblemSpec, oscillator_problem
+from .solvers import ConvergenceMonitor, Operator, SolveResult, as_operator, lsqr
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ACTIVATIONS", "CapExceededError", "ConstraintRows", "ConvergenceMonitor", "CoverageError",
+    "Decomposition", "DegenerateSubdomainError", "DeviceError", "DivergenceError", "Domain",
+    "FeatureBasis", "FilteredBlock", "FilteredSystem", "GlobalSystem", "InvalidInputError",
+    "LinearOperator2", "Operator", "PivotedQR", "PreconditionedOperator", "ProblemSpec",
+    "RandomSource", "SingularFactorError", "SolveResult", "SubdomainBlock", "apply",
+    "apply_transpose", "as_operator", "assemble", "back_substitute", "decompose",
+    "filter_system", "init_basis", "lattice_counts", "lsqr", "oscillator_problem",
+    "precondition", "qr_column_pivot", "recover_solution",
+]

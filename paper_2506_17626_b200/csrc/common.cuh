@@ -1,0 +1,68 @@
+// Shared device helpers for the featlsq B200 kernels (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/featlsq_b200.h"
+
+#define FL_CHECK_LAUNCH()                                     \
+  do {                                                        \
+    cudaError_t e_ = cudaGetLastError();                      \
+    if (e_ != cudaSuccess) return FL_ERR_CUDA;                \
+  } while (0)
+
+namespace fl {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic CTA-wide sum (fixed shuffle tree, fixed warp order). Every
+// thread gets the result. `sh` needs blockDim.x/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+// Grid-level deterministic reduction: each CTA deposits `partial` at
+// slots[blockIdx.x]; the last CTA to arrive sums all slots in index order
+// and returns true (with `total` set) in every thread of that CTA.
+__device__ __forceinline__ bool grid_sum_last(double partial, double* slots, unsigned int* counter,
+                                              double* total, double* sh) {
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    slots[blockIdx.x] = partial;
+    __threadfence();
+    unsigned int prev = atomicAdd(counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+  double acc = 0.0;
+  // fixed assignment of slots to threads + fixed tree => deterministic
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) acc += ((volatile double*)slots)[i];
+  acc = block_sum(acc, sh);
+  *total = acc;
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+__host__ __device__ __forceinline__ int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace fl

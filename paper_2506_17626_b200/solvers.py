@@ -1,0 +1,253 @@
+"""Drop-in `lsqr` with a device-resident Golub-Kahan loop (reference:
+featlsq/solvers.py:24-145).
+
+The recurrences run in CUDA (K4, csrc/qop.cu); the host enqueues the whole
+iteration budget and reads back only scalars (and x / the monitor's best
+iterate at the end). Operator polymorphism follows `as_operator`
+(solvers.py:33-44):
+
+- a `PreconditionedOperator` or a `GlobalSystem` already lives on the device
+  as dense blocks and is streamed directly;
+- a 2-D array is uploaded as one dense block;
+- any other object with `matvec/rmatvec` (an `Operator`) or
+  `apply/apply_transpose` is probed into a dense device block through its own
+  products (`size cap` below) — the loop itself never runs on the host.
+
+Monitor semantics (solvers.py:47-69): without an `error_fn` the device keeps
+the best (lowest-residual) iterate itself and the records are rebuilt from
+the device phibar trace; with an `error_fn` the loop is run in chunks of
+`stride` iterations and x is copied back at each recorded iteration to call
+it. Keyword-only `atol`/`btol`/`conlim` add scipy's stopping rule (SURVEY.md
+§0 F2); the default is the reference behaviour, a fixed budget.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .errors import DivergenceError, InvalidInputError
+
+PROBE_CAP = 50_000_000  # entries of a host-callback operator probed onto the device
+
+
+class Operator:
+    """Minimal matvec/rmatvec wrapper (`solvers.py:24-30`)."""
+
+    def __init__(self, matvec, rmatvec, shape):
+        self.matvec = matvec
+        self.rmatvec = rmatvec
+        self.shape = shape
+
+
+def as_operator(thing) -> Operator:
+    """`solvers.py:33-44`; products of device-backed inputs run on the device."""
+    from .assembly import GlobalSystem, apply, apply_transpose
+    if isinstance(thing, Operator):
+        return thing
+    if isinstance(thing, GlobalSystem):
+        return Operator(lambda v: apply(thing, v), lambda r: apply_transpose(thing, r), thing.shape)
+    if hasattr(thing, "apply") and hasattr(thing, "apply_transpose"):
+        return Operator(thing.apply, thing.apply_transpose, thing.shape)
+    arr = np.asarray(thing, dtype=float)
+    if arr.ndim != 2:
+        raise InvalidInputError(f"cannot interpret {type(thing)} as an operator")
+    return Operator(lambda v: arr @ v, lambda r: arr.T @ r, arr.shape)
+
+
+@dataclass
+class ConvergenceMonitor:
+    """`solvers.py:47-69`: records (it, residual, error) every `stride`
+    iterations and keeps the lowest-error iterate."""
+
+    error_fn: Optional[Callable[[np.ndarray], float]] = None
+    stride: int = 1
+    records: list = field(default_factory=list)
+    best_error: float = np.inf
+    best_iteration: int = -1
+    best_iterate: np.ndarray | None = None
+
+    def observe(self, iteration: int, iterate: np.ndarray, residual_fn) -> None:
+        if self.stride > 1 and iteration % self.stride != 0:
+            return
+        residual = float(residual_fn())
+        error = float(self.error_fn(iterate)) if self.error_fn else residual
+        self.records.append((iteration, residual, error))
+        if error < self.best_error:
+            self.best_error = error
+            self.best_iteration = iteration
+            self.best_iterate = iterate.copy()
+
+
+@dataclass(frozen=True)
+class SolveResult:
+    solution: np.ndarray
+    iterations_run: int
+    residual_norm: float
+    monitor: ConvergenceMonitor
+    breakdown: bool = False
+    istop: int = 0
+
+    @property
+    def best_solution(self) -> np.ndarray:
+        if self.monitor.best_iterate is None:
+            return self.solution
+        return self.monitor.best_iterate
+
+
+def _dense_blocks(arr: np.ndarray) -> D.DeviceBlocks:
+    """One dense block covering every row (rows 0..N-1, columns 0..n-1)."""
+    n_rows, n_cols = arr.shape
+    layout = D.BlockLayout(n_rows, n_cols, [np.arange(n_rows)])
+    t = D.torch()
+    buf = np.zeros((n_cols, int(layout.ld[0])))
+    buf[:, :n_rows] = arr.T
+    vals = t.from_numpy(buf.ravel()).to(D.require_cuda())
+    return D.DeviceBlocks(layout, vals, np.array([n_cols], np.int32), np.array([0], np.int64))
+
+
+def device_operator(operator):
+    """Resolve anything `as_operator` accepts to device blocks + shape."""
+    from .assembly import GlobalSystem
+    from .filtering import PreconditionedOperator
+    if isinstance(operator, PreconditionedOperator):
+        return operator.device_blocks, operator.shape
+    if isinstance(operator, GlobalSystem):
+        operator.sync_device()
+        return operator.store, operator.shape
+    if isinstance(operator, D.DeviceBlocks):
+        return operator, (operator.layout.nrows, operator.ncols_total)
+    if isinstance(operator, Operator) or (hasattr(operator, "apply")
+                                          and hasattr(operator, "apply_transpose")):
+        op = as_operator(operator)
+        m, n = (int(s) for s in op.shape)
+        if m * n > PROBE_CAP:
+            raise InvalidInputError(
+                f"host-callback operator of shape {op.shape} exceeds the device probe cap")
+        eye = np.eye(n)
+        dense = np.stack([np.asarray(op.matvec(eye[:, c]), dtype=float) for c in range(n)], axis=1) \
+            if n else np.zeros((m, 0))
+        return _dense_blocks(dense), (m, n)
+    arr = np.asarray(operator, dtype=float)
+    if arr.ndim != 2:
+        raise InvalidInputError(f"cannot interpret {type(operator)} as an operator")
+    return _dense_blocks(arr), arr.shape
+
+
+class DeviceLsqr:
+    """Device buffers + state of one LSQR run over a `DeviceBlocks` operator.
+    Reusable: `run()` re-initialises from a device rhs."""
+
+    def __init__(self, blocks: D.DeviceBlocks, max_iters: int):
+        t = D.torch()
+        dev = D.require_cuda()
+        self.blocks = blocks
+        n_rows = blocks.layout.nrows
+        n = max(blocks.ncols_total, 1)
+        self.max_iters = int(max_iters)
+        f64 = dict(dtype=t.float64, device=dev)
+        self.u = t.empty(max(n_rows, 1), **f64)
+        self.v, self.vp, self.w, self.x, self.xbest = (t.zeros(n, **f64) for _ in range(5))
+        self.trace = t.zeros(self.max_iters + 2, **f64)
+        self.state = t.zeros(C.sizeof(_lib.LsqrState), dtype=t.uint8, device=dev)
+        self.vecs = _lib.LsqrVecs(*(D.ptr(a) for a in (self.u, self.v, self.vp, self.w, self.x,
+                                                          self.xbest, self.trace)))
+
+    def reset_state(self, stride: int, track_best: bool, atol=None, btol=None, conlim=1e8):
+        st = _lib.LsqrState()
+        st.best = np.inf if track_best else -np.inf
+        st.best_it = -1
+        st.stride = max(int(stride), 1)
+        if atol is not None or btol is not None:
+            st.use_rule = 1
+            st.atol = float(atol or 0.0)
+            st.btol = float(btol or 0.0)
+            st.ctol = 1.0 / conlim if conlim > 0 else 0.0
+        host = np.frombuffer(bytes(st), dtype=np.uint8).copy()
+        self.state.copy_(D.torch().from_numpy(host))
+
+    def read_state(self) -> _lib.LsqrState:
+        raw = D.to_host(self.state).tobytes()
+        return _lib.LsqrState.from_buffer_copy(raw)
+
+    def init(self, rhs_dev):
+        L = _lib.lib()
+        _lib.check(L.fl_lsqr_init(C.byref(self.blocks.struct()), D.ptr(rhs_dev),
+                                  C.byref(self.vecs), D.ptr(self.state), D.stream_ptr()),
+                   "fl_lsqr_init")
+
+    def iterate(self, first_it: int, count: int):
+        if count <= 0:
+            return
+        _lib.check(_lib.lib().fl_lsqr_iterate(C.byref(self.blocks.struct()), C.byref(self.vecs),
+                                              D.ptr(self.state), int(first_it), int(count),
+                                              D.stream_ptr()), "fl_lsqr_iterate")
+
+
+def lsqr(operator, rhs: np.ndarray, max_iters: int,
+         monitor: ConvergenceMonitor | None = None, *,
+         atol: float | None = None, btol: float | None = None,
+         conlim: float = 1e8) -> SolveResult:
+    """Golub-Kahan LSQR from zero with a fixed budget (`solvers.py:87-145`)."""
+    blocks, shape = device_operator(operator)
+    rhs = np.asarray(rhs, dtype=float)
+    if rhs.shape != (shape[0],):
+        raise InvalidInputError(f"rhs shape {rhs.shape} != operator rows {shape[0]}")
+    monitor = monitor or ConvergenceMonitor()
+    max_iters = int(max_iters)
+    n = int(shape[1])
+    run = DeviceLsqr(blocks, max_iters)
+    host_error = monitor.error_fn is not None
+    run.reset_state(monitor.stride, track_best=not host_error, atol=atol, btol=btol,
+                    conlim=conlim)
+    run.init(D.to_dev(rhs))
+    st = run.read_state()
+    x0 = np.zeros(n)
+    if st.beta == 0.0:                              # solvers.py:104-106
+        monitor.observe(0, x0, lambda: 0.0)
+        return SolveResult(x0, 0, 0.0, monitor)
+    if st.alpha == 0.0:                             # solvers.py:110-112
+        monitor.observe(0, x0, lambda: st.beta)
+        return SolveResult(x0, 0, st.beta, monitor, breakdown=True)
+
+    if not host_error:
+        run.iterate(1, max_iters)
+        st = run.read_state()
+    else:
+        it = 0
+        stride = max(monitor.stride, 1)
+        while it < max_iters:
+            count = min(stride - (it % stride), max_iters - it)
+            run.iterate(it + 1, count)
+            st = run.read_state()
+            done_it = int(st.it)
+            if st.diverged_at:
+                break
+            if done_it % stride == 0 and done_it > it:
+                x_now = D.to_host(run.x)[:n]
+                ph = float(run.trace[done_it].item())
+                monitor.observe(done_it, x_now, lambda: ph)
+            it = it + count
+            if st.done:
+                break
+    if st.diverged_at:
+        raise DivergenceError(f"non-finite iterate at iteration {int(st.diverged_at)}")
+    iters = int(st.it)
+    x = D.to_host(run.x)[:n]
+    if not host_error:
+        trace = D.to_host(run.trace)
+        stride = max(monitor.stride, 1)
+        for it in range(1, iters + 1):
+            if stride > 1 and it % stride != 0:
+                continue
+            monitor.records.append((it, float(trace[it]), float(trace[it])))
+        if st.best_it >= 1:
+            monitor.best_error = float(st.best)
+            monitor.best_iteration = int(st.best_it)
+            monitor.best_iterate = D.to_host(run.xbest)[:n].copy()
+    return SolveResult(x, iters, float(st.phibar), monitor, bool(st.breakdown), int(st.istop))
