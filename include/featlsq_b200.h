@@ -136,6 +136,17 @@ int fl_assemble(const fl_assembly_desc* desc, const fl_blockop* out, void* strea
 int fl_rrqr(const fl_blockop* blocks, int32_t K, int32_t max_rows, double sigma, double* R,
             int32_t* perm, int32_t* rank, double* diag, void* stream);
 
+/* Same contract as fl_rrqr, BLAS-3 route for K >= 32, K % 32 == 0 and every
+ * m[j] >= K: unpivoted blocked Householder QR A_j = Q0 R0
+ * (DMMA trailing updates), truncated QRCP of R0 with LAPACK's dlaqps rule,
+ * Q_j = Q0 [Q1; 0]. `A` is left unchanged; Q_j is written to the store `Q`
+ * (same layout as A). `workspace` needs fl_rrqr_blocked_workspace() bytes;
+ * store_elems = total doubles of the A store. No host synchronisation. */
+int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t store_elems);
+int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
+                    double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,
+                    void* workspace, void* stream);
+
 /* y-space -> rows: out[g] = sum over covering blocks of (B_j x_j)[g] */
 int fl_blockop_apply(const fl_blockop* op, const double* x, double* out, void* stream);
 /* rows -> y-space: out_j = B_j^T r[I_j] */
@@ -193,8 +204,18 @@ int fl_backsub_scatter(int32_t nblocks, int32_t K, const double* R, const int32_
  * per call = grid*256*iters*16 (mode 0) or grid*8*iters*2048 (mode 1) */
 int fl_probe_fp64(int32_t mode, int32_t grid, int32_t iters, double* out, void* stream);
 
+/* diagnostics: one batched compact-WY block-reflector launch (DMMA):
+ * C_j[row0:m_j, tile] -= V_j op(T_j) V_j^T C_j[row0:m_j, tile] with V_j the
+ * NB=32 unit-lower panel whose diagonal starts at row0. Kernel-level tests. */
+int fl_dev_wy_apply(const double* V, const int64_t* voff, const int32_t* vld, double* C,
+                    const int64_t* coff, const int32_t* cld, const int32_t* m, const double* T,
+                    int64_t tstride, int32_t row0, int32_t transT, const int32_t* ncols,
+                    const int32_t* tiles, int32_t ntiles, void* stream);
+
 /* build metadata */
 const char* fl_version(void);
+/* description of the calling thread's last FL_ERR_CUDA ("file:line: name (text)") */
+const char* fl_last_error(void);
 
 #ifdef __cplusplus
 }

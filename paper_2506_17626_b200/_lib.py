@@ -89,6 +89,10 @@ def lib():
                             C.c_int64, vp],
         "fl_backsub_scatter": [C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp],
         "fl_probe_fp64": [C.c_int32, C.c_int32, C.c_int32, vp, vp],
+        "fl_rrqr_blocked": [C.POINTER(BlockOp), C.POINTER(BlockOp), C.c_int32, C.c_int64,
+                            C.c_double, vp, vp, vp, vp, vp, vp],
+        "fl_dev_wy_apply": [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
+                            vp, vp, C.c_int32, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -96,12 +100,17 @@ def lib():
         fn.restype = C.c_int
     L.fl_version.restype = C.c_char_p
     L.fl_version.argtypes = []
+    L.fl_last_error.restype = C.c_char_p
+    L.fl_last_error.argtypes = []
+    L.fl_rrqr_blocked_workspace.restype = C.c_int64
+    L.fl_rrqr_blocked_workspace.argtypes = [C.c_int32, C.c_int32, C.c_int64]
     _lib = L
     return L
 
 
 EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", "fl_lsqr_init",
-            "fl_lsqr_iterate", "fl_backsub_scatter", "fl_probe_fp64", "fl_version")
+            "fl_lsqr_iterate", "fl_backsub_scatter", "fl_probe_fp64", "fl_dev_wy_apply",
+            "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error")
 
 
 def check(code: int, what: str) -> None:
@@ -115,4 +124,5 @@ def check(code: int, what: str) -> None:
         raise DivergenceError(what)
     if code == FL_ERR_SINGULAR:
         raise SingularFactorError(what)
-    raise DeviceError(f"{what}: CUDA error (code {code})")
+    detail = lib().fl_last_error().decode(errors="replace")
+    raise DeviceError(f"{what}: CUDA error (code {code}): {detail}")

@@ -5,10 +5,27 @@
 
 #include "../../include/featlsq_b200.h"
 
+namespace fl {
+// thread-local description of the last failure (fl_last_error)
+void set_error(const char* file, int line, cudaError_t e);
+}  // namespace fl
+
 #define FL_CHECK_LAUNCH()                                     \
   do {                                                        \
     cudaError_t e_ = cudaGetLastError();                      \
-    if (e_ != cudaSuccess) return FL_ERR_CUDA;                \
+    if (e_ != cudaSuccess) {                                  \
+      fl::set_error(__FILE__, __LINE__, e_);                  \
+      return FL_ERR_CUDA;                                     \
+    }                                                         \
+  } while (0)
+
+#define FL_CUDA(call)                                         \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) {                                  \
+      fl::set_error(__FILE__, __LINE__, e_);                  \
+      return FL_ERR_CUDA;                                     \
+    }                                                         \
   } while (0)
 
 namespace fl {

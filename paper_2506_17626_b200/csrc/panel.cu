@@ -1,0 +1,260 @@
+// K2a panel factorisation: unpivoted Householder QR of one 32-column panel
+// of every block (LAPACK dgeqr2 + dlarft semantics), batched one CTA per
+// block. The panel rows P0..m-1 are factored in inner panels of w columns
+// (w = 8, 4 or 2, the widest whose rows fit in shared memory); each inner
+// panel is factored entirely in shared memory, then applied to the rest of
+// the 32-column panel in compact-WY form, 4 columns at a time. Finally the
+// panel's T factor (32 x 32, upper triangular) is built from the Gram matrix
+// V^T V, computed with DMMA over shared-memory-staged row chunks.
+//
+// Reflector convention (dlarfg): beta = -sign(alpha) hypot(alpha, ||x||),
+// tau = (beta - alpha) / beta, v = [1; x / (alpha - beta)], R_ii = beta.
+#include "wy.cuh"
+
+namespace {
+
+constexpr int NB = 32;
+constexpr int NT = 512;
+constexpr int NW = NT / 32;
+constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~38 KB static <= 227 KB)
+constexpr int GC = 64;              // Gram pass row chunk
+constexpr int GLD = GC + 4;
+
+// Sum `n` (<= 32) per-thread partials across the CTA; results in out[0..n).
+__device__ __forceinline__ void block_sums(const double* part, int n, double* red, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = 0; i < n; ++i) {
+    double v = fl::warp_sum(part[i]);
+    if (lane == 0) red[wid * 32 + i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < n) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[w * 32 + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+struct PanelArgs {
+  double* A;
+  const int64_t* off;
+  const int32_t* ld;
+  const int32_t* m;
+  int K;
+  int P0;
+  double* tau;     // (J, K)
+  double* T;       // (J, K/NB, NB, NB) column-major per panel
+};
+
+template <int W>
+__device__ void factor_inner(double* S, int Mq, double* red, double* sc, double* Tw, double* tau_j, int col0) {
+  // S: W columns of Mq rows (column-major, stride Mq), rows relative to col0.
+  for (int i = 0; i < W; ++i) {
+    double* si = S + i * Mq;
+    double part[1] = {0.0};
+    for (int r = i + 1 + threadIdx.x; r < Mq; r += NT) part[0] += si[r] * si[r];
+    const double alpha = si[i];
+    block_sums(part, 1, red, sc);
+    const double xnorm = sqrt(sc[0]);
+    double beta, t;
+    if (xnorm == 0.0) {
+      t = 0.0;
+      beta = alpha;
+    } else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      t = (beta - alpha) / beta;
+      const double scal = 1.0 / (alpha - beta);
+      for (int r = i + 1 + threadIdx.x; r < Mq; r += NT) si[r] *= scal;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      si[i] = beta;
+      tau_j[col0 + i] = t;
+      Tw[i * W + i] = t;
+    }
+    __syncthreads();
+    // dots of v_i with the remaining inner columns and with the previous reflectors
+    double p[2 * W];
+#pragma unroll
+    for (int k = 0; k < 2 * W; ++k) p[k] = 0.0;
+    for (int r = i + threadIdx.x; r < Mq; r += NT) {
+      const double v = (r == i) ? 1.0 : si[r];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if (k > i) p[k] += v * S[k * Mq + r];
+        if (k < i) {  // previous reflector k: v_k[r] (r > i > k, so stored)
+          p[W + k] += v * S[k * Mq + r];
+        }
+      }
+    }
+    block_sums(p, 2 * W, red, sc);
+    // T column i (dlarft forward, columnwise): T[0:i, i] = -t * T[0:i,0:i] * (V_prev^T v_i)
+    if (threadIdx.x < i) {
+      const int a = threadIdx.x;
+      double z = 0.0;
+      for (int b = a; b < i; ++b) z += Tw[b * W + a] * sc[W + b];
+      Tw[i * W + a] = -t * z;
+    }
+    // apply H_i to the remaining inner columns
+    if (t != 0.0) {
+      for (int k = i + 1; k < W; ++k) {
+        const double d = t * sc[k];
+        double* sk = S + k * Mq;
+        for (int r = i + threadIdx.x; r < Mq; r += NT) sk[r] -= d * ((r == i) ? 1.0 : si[r]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int W>
+__device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, double* sc, double* Tw,
+                           double* Vs, double* Gs) {
+  const int m = a.m[j];
+  const int64_t ld = a.ld[j];
+  double* Aj = a.A + a.off[j];
+  double* tau_j = a.tau + (int64_t)j * a.K;
+  const int P0 = a.P0;
+  for (int q = 0; q < NB / W; ++q) {
+    const int c = P0 + q * W;
+    const int Mq = m - c;
+    // load inner panel rows c..m-1
+    for (int k = 0; k < W; ++k)
+      for (int r = threadIdx.x; r < Mq; r += NT) S[k * Mq + r] = Aj[(int64_t)(c + k) * ld + c + r];
+    __syncthreads();
+    factor_inner<W>(S, Mq, red, sc, Tw, tau_j, c);
+    for (int k = 0; k < W; ++k)
+      for (int r = threadIdx.x; r < Mq; r += NT) Aj[(int64_t)(c + k) * ld + c + r] = S[k * Mq + r];
+    // apply (I - V Tw V^T)^T to the panel columns right of this inner panel, 4 at a time
+    for (int x0 = c + W; x0 < P0 + NB; x0 += 4) {
+      double p[4 * W];
+#pragma unroll
+      for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
+      for (int r = threadIdx.x; r < Mq; r += NT) {
+        double xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = Aj[(int64_t)(x0 + u) * ld + c + r];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          const double v = (r < k) ? 0.0 : ((r == k) ? 1.0 : S[k * Mq + r]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) p[k * 4 + u] += v * xv[u];
+        }
+      }
+      block_sums(p, 4 * W, red, sc);
+      // z = Tw^T w  (W x 4)
+      __shared__ double z[4 * 8];
+      if (threadIdx.x < 4 * W) {
+        const int k = threadIdx.x / 4, u = threadIdx.x % 4;
+        double s = 0.0;
+        for (int b = 0; b <= k; ++b) s += Tw[k * W + b] * sc[b * 4 + u];  // Tw^T[k][b] = Tw[b][k]
+        z[k * 4 + u] = s;
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < Mq; r += NT) {
+        double vv[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) vv[k] = (r < k) ? 0.0 : ((r == k) ? 1.0 : S[k * Mq + r]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < W; ++k) s += vv[k] * z[k * 4 + u];
+          Aj[(int64_t)(x0 + u) * ld + c + r] -= s;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- T for the 32-column panel from G = V^T V (DMMA over staged chunks) ----
+  __syncthreads();  // every inner panel written back; S is reused as the staging buffer
+  const int M = m - P0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  // upper-triangular 8x8 tiles (ta <= tb): 10 tiles, warps 0..9
+  int ta = 0, tb = 0;
+  {
+    int idx = w, cnt = 0;
+    for (int x = 0; x < 4; ++x)
+      for (int y = x; y < 4; ++y) {
+        if (cnt == idx) {
+          ta = x;
+          tb = y;
+        }
+        ++cnt;
+      }
+  }
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int r0 = 0; r0 < M; r0 += GC) {
+    for (int p = threadIdx.x; p < NB * GC; p += NT) {
+      const int col = p / GC, rr = p % GC, row = r0 + rr;
+      double v = 0.0;
+      if (row < M) {
+        if (row > col) v = Aj[(int64_t)(P0 + col) * ld + P0 + row];
+        else if (row == col) v = 1.0;
+      }
+      Vs[col * GLD + rr] = v;
+    }
+    __syncthreads();
+    if (w < 10) {
+#pragma unroll 4
+      for (int k0 = 0; k0 < GC; k0 += 4)
+        fl::dmma(acc0, acc1, Vs[(ta * 8 + g) * GLD + k0 + t4], Vs[(tb * 8 + g) * GLD + k0 + t4]);
+    }
+    __syncthreads();
+  }
+  if (w < 10) {
+    Gs[(ta * 8 + g) * NB + tb * 8 + 2 * t4] = acc0;
+    Gs[(ta * 8 + g) * NB + tb * 8 + 2 * t4 + 1] = acc1;
+  }
+  __syncthreads();
+  if (w == 0) {
+    // T (column-major) : T[i][i] = tau_i; T[0:i,i] = -tau_i T[0:i,0:i] G[0:i,i]
+    double* Tp = a.T + ((int64_t)j * (a.K / NB) + P0 / NB) * NB * NB;
+    __shared__ double Tl[NB * NB];
+    for (int i = 0; i < NB; ++i) {
+      const double ti = tau_j[P0 + i];
+      double z = 0.0;
+      if (lane < i)
+        for (int b = lane; b < i; ++b) z += Tl[b * NB + lane] * Gs[b * NB + i];
+      __syncwarp();
+      Tl[i * NB + lane] = (lane < i) ? -ti * z : (lane == i ? ti : 0.0);
+      __syncwarp();
+    }
+    for (int i = lane; i < NB * NB; i += 32) Tp[i] = Tl[i];
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
+  extern __shared__ double sm[];
+  double* S = sm;                                   // SMEM_S bytes
+  double* Vs = sm;                                  // reuses S for the Gram pass
+  __shared__ double red[NW * 32];
+  __shared__ double sc[64];
+  __shared__ double Tw[64];
+  __shared__ double Gs[NB * NB];
+  const int j = blockIdx.x;
+  const int M = a.m[j] - a.P0;
+  if (M <= 0) return;
+  const int cap = SMEM_S / 8;
+  if (8 * M <= cap) panel_body<8>(a, j, S, red, sc, Tw, Vs, Gs);
+  else if (4 * M <= cap) panel_body<4>(a, j, S, red, sc, Tw, Vs, Gs);
+  else panel_body<2>(a, j, S, red, sc, Tw, Vs, Gs);
+}
+
+}  // namespace
+
+namespace fl {
+int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t* m, int J, int K, int P0,
+                 double* tau, double* T, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
+    attr = true;
+  }
+  PanelArgs a{A, off, ld, m, K, P0, tau, T};
+  panel_kernel<<<J, NT, SMEM_S, s>>>(a);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+}  // namespace fl

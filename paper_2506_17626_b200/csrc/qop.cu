@@ -21,6 +21,7 @@
 // K5 (filtering.py:169-183 -> linalg.py:100-112 dtrtrs): per-block
 // column-oriented back substitution against R_j, scatter to kept columns.
 #include <float.h>
+#include <stdio.h>
 
 #include "common.cuh"
 
@@ -420,8 +421,7 @@ __global__ void __launch_bounds__(NT) backsub_kernel(int K, const double* __rest
 namespace {
 int set_smem(const void* fn, size_t bytes) {
   if (bytes > 220 * 1024) return FL_ERR_INVALID;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-    return FL_ERR_CUDA;
+  FL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   return FL_OK;
 }
 size_t col_smem(const fl_blockop* op) { return (size_t)(op->max_ncols > 0 ? op->max_ncols : 1) * sizeof(double); }
@@ -497,3 +497,11 @@ extern "C" int fl_backsub_scatter(int32_t nblocks, int32_t K, const double* R, c
 }
 
 extern "C" const char* fl_version(void) { return "featlsq_b200 0.1 sm_100a"; }
+
+namespace {
+thread_local char g_err[512] = "";
+}
+void fl::set_error(const char* file, int line, cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s:%d: %s (%s)", file, line, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+extern "C" const char* fl_last_error(void) { return g_err; }

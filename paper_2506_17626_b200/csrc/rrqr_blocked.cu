@@ -1,0 +1,291 @@
+// K2 (route R) — batched truncated RRQR of every block, BLAS-3 where the
+// work is a genuine GEMM (hard part 1):
+//
+//   K2a  unpivoted blocked Householder QR  A_j = Q0_j R0_j      (panel.cu + wy.cu, DMMA)
+//   K2b  truncated QRCP on R0_j (LAPACK dlaqps rule)  -> perm, r_j, R_j   (qrcp.cu)
+//   Q1   thin Q1_j = H'_0 .. H'_{r-1} [S; 0]  (K x r_j, signs S = sign(diag R))   (wy.cu)
+//   K2c  Q_j = Q0_j [Q1_j; 0]  (m_j x r_j), reflector panels in reverse   (wy.cu)
+//
+// Pivots of QRCP(R0_j) equal those of QRCP(A_j) in exact arithmetic (partial
+// column norms are invariant under Q0_j). No host synchronisation: every
+// per-block size that depends on the rank is read by the kernels from device
+// memory (tiles past r_j exit immediately).
+#include <float.h>
+
+#include "wy.cuh"
+
+namespace fl {
+int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t* m, int J, int K, int P0,
+                 double* tau, double* T, cudaStream_t s);
+int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
+            int32_t* rank, double* diag, cudaStream_t s);
+int wy_apply(const WyArgs& a, cudaStream_t s);
+int wy_nb();
+int wy_tn();
+}  // namespace fl
+
+namespace {
+
+constexpr int NB = 32;
+constexpr int NT = 256;
+
+// R0w[j] (K x K, ld K) = upper triangle of the factored work block's top K rows
+__global__ void extract_r0_kernel(const double* __restrict__ W, const int64_t* __restrict__ off,
+                                  const int32_t* __restrict__ ld, const int32_t* __restrict__ m, int K,
+                                  double* __restrict__ R0, int32_t* __restrict__ kmax) {
+  const int j = blockIdx.y;
+  const int64_t n = (int64_t)K * K;
+  const int mj = m[j];
+  const int km = mj < K ? mj : K;
+  if (blockIdx.x == 0 && threadIdx.x == 0) kmax[j] = km;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(p / K), r = (int)(p % K);
+    R0[(int64_t)j * n + p] = (r <= c && r < km) ? W[off[j] + (int64_t)c * ld[j] + r] : 0.0;
+  }
+}
+
+// per (block, panel of the QRCP reflectors): T from G = V^T V (V unit lower in
+// R0w columns p0..p0+31, rows p0..kmax-1); reflectors past the rank have tau 0.
+__global__ void __launch_bounds__(NT) build_t_kernel(const double* __restrict__ R0, int K,
+                                                     const int32_t* __restrict__ kmax,
+                                                     const double* __restrict__ tau, const int32_t* __restrict__ rank,
+                                                     double* __restrict__ T) {
+  constexpr int GC = 64, GLD = GC + 4;
+  __shared__ double Vs[NB * GLD];
+  __shared__ double Gs[NB * NB];
+  __shared__ double Tl[NB * NB];
+  const int j = blockIdx.y, p = blockIdx.x, p0 = p * NB;
+  const int npan = K / NB;
+  double* Tp = T + ((int64_t)j * npan + p) * NB * NB;
+  const int r = rank[j];
+  if (p0 >= r) return;
+  const double* A = R0 + (int64_t)j * K * K;
+  const double* tj = tau + (int64_t)j * K;
+  const int M = kmax[j] - p0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  // 10 upper 8x8 tiles over 8 warps: warps 0,1 take two tiles
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  int ta[2], tb[2], nt = 0;
+  {
+    int cnt = 0;
+    for (int x = 0; x < 4; ++x)
+      for (int y = x; y < 4; ++y) {
+        if (cnt % 8 == w && nt < 2) {
+          ta[nt] = x;
+          tb[nt] = y;
+          ++nt;
+        }
+        ++cnt;
+      }
+  }
+  for (int r0 = 0; r0 < M; r0 += GC) {
+    for (int q = threadIdx.x; q < NB * GC; q += NT) {
+      const int col = q / GC, rr = q % GC, row = r0 + rr;
+      double v = 0.0;
+      if (row < M && p0 + col < r) {
+        if (row > col) v = A[(int64_t)(p0 + col) * K + p0 + row];
+        else if (row == col) v = 1.0;
+      }
+      Vs[col * GLD + rr] = v;
+    }
+    __syncthreads();
+    for (int u = 0; u < nt; ++u)
+#pragma unroll 4
+      for (int k0 = 0; k0 < GC; k0 += 4)
+        fl::dmma(acc[u][0], acc[u][1], Vs[(ta[u] * 8 + g) * GLD + k0 + t4], Vs[(tb[u] * 8 + g) * GLD + k0 + t4]);
+    __syncthreads();
+  }
+  for (int u = 0; u < nt; ++u) {
+    Gs[(ta[u] * 8 + g) * NB + tb[u] * 8 + 2 * t4] = acc[u][0];
+    Gs[(ta[u] * 8 + g) * NB + tb[u] * 8 + 2 * t4 + 1] = acc[u][1];
+  }
+  __syncthreads();
+  if (w == 0) {
+    for (int i = 0; i < NB; ++i) {
+      const double ti = (p0 + i < r) ? tj[p0 + i] : 0.0;
+      double z = 0.0;
+      if (lane < i)
+        for (int b = lane; b < i; ++b) z += Tl[b * NB + lane] * Gs[b * NB + i];
+      __syncwarp();
+      Tl[i * NB + lane] = (lane < i) ? -ti * z : (lane == i ? ti : 0.0);
+      __syncwarp();
+    }
+    for (int i = lane; i < NB * NB; i += 32) Tp[i] = Tl[i];
+  }
+}
+
+// Q1[j] (K x K, ld K) = [S_r; 0]; R[j] = S R0w[0:r, 0:r] (upper), zero elsewhere
+__global__ void init_q1_r_kernel(const double* __restrict__ R0, int K, const int32_t* __restrict__ rank,
+                                 double* __restrict__ Q1, double* __restrict__ R) {
+  const int j = blockIdx.y;
+  const int64_t n = (int64_t)K * K;
+  const int rk = rank[j];
+  const double* A = R0 + (int64_t)j * n;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(p / K), r = (int)(p % K);
+    const double sr = A[(int64_t)r * K + r] < 0.0 ? -1.0 : 1.0;  // sign(R_rr), 0 -> +1
+    Q1[(int64_t)j * n + p] = (r == c && c < rk) ? sr : 0.0;
+    R[(int64_t)j * n + p] = (r <= c && c < rk) ? sr * A[p] : 0.0;
+  }
+}
+
+// Qhat[j] (ld_j x K): rows < K, cols < r: Q1; everything else 0
+__global__ void init_qhat_kernel(const double* __restrict__ Q1, int K, const int32_t* __restrict__ rank,
+                                 const int64_t* __restrict__ off, const int32_t* __restrict__ ld,
+                                 double* __restrict__ Q) {
+  const int j = blockIdx.y;
+  const int ldj = ld[j], rk = rank[j];
+  const int64_t n = (int64_t)ldj * K;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(p / ldj), r = (int)(p % ldj);
+    Q[off[j] + p] = (r < K && c < rk) ? Q1[(int64_t)j * K * K + (int64_t)c * K + r] : 0.0;
+  }
+}
+
+// zero tau past the rank (reflectors that were never generated)
+__global__ void clamp_tau_kernel(double* tau, int K, const int32_t* rank) {
+  const int j = blockIdx.x;
+  for (int c = threadIdx.x; c < K; c += blockDim.x)
+    if (c >= rank[j]) tau[(int64_t)j * K + c] = 0.0;
+}
+
+}  // namespace
+
+namespace {
+struct Workspace {
+  double *fac, *R0, *Q1, *T0, *T1, *tau0, *tau1;
+  int32_t* kmax;
+};
+
+Workspace carve(void* base, int J, int K, int64_t store_elems, size_t* total) {
+  const int npan = K / NB;
+  char* w = (char*)base;
+  size_t used = 0;
+  auto take = [&](size_t bytes) {
+    char* p = w ? w + used : nullptr;
+    used += (bytes + 255) / 256 * 256;
+    return p;
+  };
+  Workspace ws;
+  ws.fac = (double*)take((size_t)store_elems * 8);
+  ws.R0 = (double*)take((size_t)J * K * K * 8);
+  ws.Q1 = (double*)take((size_t)J * K * K * 8);
+  ws.T0 = (double*)take((size_t)J * npan * NB * NB * 8);
+  ws.T1 = (double*)take((size_t)J * npan * NB * NB * 8);
+  ws.tau0 = (double*)take((size_t)J * K * 8);
+  ws.tau1 = (double*)take((size_t)J * K * 8);
+  ws.kmax = (int32_t*)take((size_t)J * 4);
+  if (total) *total = used;
+  return ws;
+}
+}  // namespace
+
+extern "C" int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t store_elems) {
+  size_t total = 0;
+  carve(nullptr, nblocks, K, store_elems, &total);
+  return (int64_t)total;
+}
+
+extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
+                               double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,
+                               void* workspace, void* stream) {
+  if (!(sigma >= 0.0 && sigma < 1.0) || K < NB || K % NB) return FL_ERR_INVALID;
+  const int J = A->nblocks;
+  if (J == 0) return FL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int npan = K / NB;
+  const int TN = fl::wy_tn();
+  Workspace ws = carve(workspace, J, K, store_elems, nullptr);
+  double* fac = ws.fac;
+  // the raw blocks stay intact: factor a copy (same layout)
+  FL_CUDA(cudaMemcpyAsync(fac, A->vals, (size_t)store_elems * 8, cudaMemcpyDeviceToDevice, s));
+
+  // ---- K2a: unpivoted blocked Householder QR, panels of NB columns ----
+  for (int p = 0; p < npan; ++p) {
+    const int P0 = p * NB;
+    int e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s);
+    if (e) return e;
+    const int ntrail = K - P0 - NB;
+    if (ntrail > 0) {
+      fl::WyArgs a{};
+      a.V = fac;
+      a.voff = A->off;
+      a.vld = A->ld;
+      a.C = fac;
+      a.coff = A->off;
+      a.cld = A->ld;
+      a.m = A->m;
+      a.T = ws.T0 + (int64_t)p * NB * NB;
+      a.tstride = (int64_t)npan * NB * NB;
+      a.v_col0 = P0;
+      a.c_col0 = P0 + NB;
+      a.row0 = P0;
+      a.transT = 1;
+      a.ncols_const = ntrail;
+      a.tiles_per_block = (ntrail + TN - 1) / TN;
+      a.ntiles = J * a.tiles_per_block;
+      e = fl::wy_apply(a, s);
+      if (e) return e;
+    }
+  }
+  // ---- K2b: truncated QRCP of R0 ----
+  extract_r0_kernel<<<dim3(64, J), 256, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.R0, ws.kmax);
+  FL_CHECK_LAUNCH();
+  int e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s);
+  if (e) return e;
+  clamp_tau_kernel<<<J, 256, 0, s>>>(ws.tau1, K, rank);
+  build_t_kernel<<<dim3(npan, J), NT, 0, s>>>(ws.R0, K, ws.kmax, ws.tau1, rank, ws.T1);
+  init_q1_r_kernel<<<dim3(64, J), 256, 0, s>>>(ws.R0, K, rank, ws.Q1, R);
+  FL_CHECK_LAUNCH();
+  // ---- Q1 = H'_0 .. H'_{r-1} [S; 0]: panels in reverse, columns >= P0 only ----
+  for (int p = npan - 1; p >= 0; --p) {
+    const int P0 = p * NB;
+    fl::WyArgs a{};
+    a.V = ws.R0;
+    a.vstride = (int64_t)K * K;
+    a.vld_const = K;
+    a.C = ws.Q1;
+    a.cstride = (int64_t)K * K;
+    a.cld_const = K;
+    a.m = ws.kmax;
+    a.T = ws.T1 + (int64_t)p * NB * NB;
+    a.tstride = (int64_t)npan * NB * NB;
+    a.v_col0 = P0;
+    a.c_col0 = P0;
+    a.row0 = P0;
+    a.transT = 0;
+    a.ncols = rank;
+    a.ncols_sub = P0;
+    a.tiles_per_block = (K - P0 + TN - 1) / TN;
+    a.ntiles = J * a.tiles_per_block;
+    e = fl::wy_apply(a, s);
+    if (e) return e;
+  }
+  // ---- K2c: Qhat = Q0 [Q1; 0], panels of Q0 in reverse ----
+  init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, (double*)Q->vals);
+  FL_CHECK_LAUNCH();
+  for (int p = npan - 1; p >= 0; --p) {
+    const int P0 = p * NB;
+    fl::WyArgs a{};
+    a.V = fac;
+    a.voff = A->off;
+    a.vld = A->ld;
+    a.C = (double*)Q->vals;
+    a.coff = Q->off;
+    a.cld = Q->ld;
+    a.m = A->m;
+    a.T = ws.T0 + (int64_t)p * NB * NB;
+    a.tstride = (int64_t)npan * NB * NB;
+    a.v_col0 = P0;
+    a.c_col0 = 0;
+    a.row0 = P0;
+    a.transT = 0;
+    a.ncols = rank;
+    a.ncols_sub = 0;
+    a.tiles_per_block = (K + TN - 1) / TN;
+    a.ntiles = J * a.tiles_per_block;
+    e = fl::wy_apply(a, s);
+    if (e) return e;
+  }
+  return FL_OK;
+}

@@ -121,14 +121,18 @@ def test_recovery_matches_oracle(fl, name):
     a_ref = O.recover_solution(fb, off, y, ref["column_count"])
     dropped = np.concatenate(fs.dropped_list)
     assert np.all(a_dev[dropped] == 0.0)
-    # recovery consistency (tests/test_filtering.py:143-149): Q y == M a for
-    # the device's own factors; across QR implementations the predicted rows
-    # differ by the Q-factor difference (~1e-6)
+    # Q y == M a holds to ~eps * kappa(R_j) (kappa(R_j) ~ 1e10 at sigma = 1e-10),
+    # for the device's factors and for the oracle's alike; the reference's own
+    # 1e-8 check (tests/test_filtering.py:143-149) is at sigma = 1e-4, see
+    # test_filter_sigma_properties
     M = O.raw_operator(ref)
     ma = M @ a_dev
     qy = fl.precondition(fs).apply(y)
-    assert np.linalg.norm(ma - qy) <= 1e-8 * np.linalg.norm(qy)
     mr = M @ a_ref
+    qr = O.q_operator(fb, off, ref["row_count"]) @ y
+    dev_gap = np.linalg.norm(ma - qy) / np.linalg.norm(qy)
+    ref_gap = np.linalg.norm(mr - qr) / np.linalg.norm(qr)
+    assert dev_gap <= 1e-5 and dev_gap <= 10 * max(ref_gap, 1e-12)
     assert np.linalg.norm(ma - mr) <= 1e-5 * np.linalg.norm(mr)
     # identical factor: device back substitution == scipy dtrtrs to 1e-12
     for blk in list(fs.blocks)[:4]:
@@ -335,6 +339,10 @@ def test_filter_sigma_properties(fl):
     y = np.concatenate([b.r_factor @ a_true[b.kept_columns] for b in fs.blocks])
     assert np.allclose(fl.recover_solution(fs, y), a_true, atol=1e-8)
     op = fl.precondition(fs)
+    # tests/test_filtering.py:143-149: Q y and M a agree when a = recover(y)
+    yy = np.random.default_rng(6).standard_normal(loose.kept_total)
+    assert np.allclose(fl.precondition(loose).apply(yy),
+                       fl.apply(system, fl.recover_solution(loose, yy)), atol=1e-8)
     import scipy.linalg
     s_inv = scipy.linalg.block_diag(*[np.linalg.inv(b.r_factor) for b in loose.blocks])
     assert np.allclose(fl.precondition(loose).materialize(), loose.materialize() @ s_inv, atol=1e-10)
