@@ -206,10 +206,10 @@ int fl_probe_fp64(int32_t mode, int32_t grid, int32_t iters, double* out, void* 
 
 /* diagnostics: one batched compact-WY block-reflector launch (DMMA):
  * C_j[row0:m_j, tile] -= V_j op(T_j) V_j^T C_j[row0:m_j, tile] with V_j the
- * NB=32 unit-lower panel whose diagonal starts at row0. Kernel-level tests. */
+ * nb-wide (32 or 64) unit-lower panel whose diagonal starts at row0. */
 int fl_dev_wy_apply(const double* V, const int64_t* voff, const int32_t* vld, double* C,
                     const int64_t* coff, const int32_t* cld, const int32_t* m, const double* T,
-                    int64_t tstride, int32_t row0, int32_t transT, const int32_t* ncols,
+                    int64_t tstride, int32_t nb, int32_t row0, int32_t transT, const int32_t* ncols,
                     const int32_t* tiles, int32_t ntiles, void* stream);
 
 /* build metadata */

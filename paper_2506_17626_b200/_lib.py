@@ -92,7 +92,7 @@ def lib():
         "fl_rrqr_blocked": [C.POINTER(BlockOp), C.POINTER(BlockOp), C.c_int32, C.c_int64,
                             C.c_double, vp, vp, vp, vp, vp, vp],
         "fl_dev_wy_apply": [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
-                            vp, vp, C.c_int32, vp],
+                            C.c_int32, vp, vp, C.c_int32, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -1,8 +1,8 @@
 // K2b — truncated column-pivoted QR of the triangular factor R0_j of every
 // block (route R: QRCP(A_j) and QRCP(R0_j) choose the same pivots in exact
 // arithmetic because partial column norms are invariant under the
-// orthogonal Q0_j). One CTA per block, R0_j (K x K,
-// column-major, ld K) in HBM/L2.
+// orthogonal Q0_j). One CTA per block (256 threads, two CTAs
+// per SM), R0_j (K x K, column-major, ld K) streamed from HBM/L2.
 //
 // Pivot rule and norm bookkeeping follow LAPACK's blocked dlaqps (what
 // dgeqp3 runs on the leading columns): first maximum of the partial norms
@@ -12,15 +12,21 @@
 // columns with temp * (vn1/vn2)^2 <= sqrt(eps) flagged and the panel closed
 // early, their norms recomputed after the block update. Truncation: the
 // first step with |R_ii| < sigma |R_00| stops everything (linalg.py:75-85).
+//
+// The step's critical path is a handful of dependent memory round trips, so
+// the kernel is organised for memory-level parallelism: the column swap is
+// fused with the pivot column's panel update, the F-gemv keeps four columns
+// in flight per warp, and row i of the trailing columns is prefetched while
+// the F-gemv runs.
 #include <float.h>
 
 #include "wy.cuh"
 
 namespace {
 
-constexpr int NT = 512;
+constexpr int NT = 256;
 constexpr int NW = NT / 32;
-constexpr int PB = 32;  // panel width
+constexpr int PB = 16;  // panel width (F has PB columns)
 
 struct QrcpArgs {
   double* R0;          // (J, K, K) column-major, ld K; on exit: R above, reflectors below
@@ -45,35 +51,25 @@ __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
   }
 }
 
-__device__ __forceinline__ double blk_sum(double x, double* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  x = fl::warp_sum(x);
-  if (lane == 0) red[wid] = x;
-  __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < NW; ++w) s += red[w];
-  __syncthreads();
-  return s;
-}
-
-__global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
+__global__ void __launch_bounds__(NT, 2) qrcp_kernel(QrcpArgs q) {
   extern __shared__ double sm[];
   const int K = q.K;
   const int j = blockIdx.x;
-  const int M = q.kmax[j];   // rows of R0 that matter
+  const int M = q.kmax[j];
   const int N = K;
-  double* F = sm;                    // [PB][K]  (column-major: F[k*K + c])
+  double* F = sm;                    // [PB][K]  F[k*K + c]
   double* vn1 = F + PB * K;
   double* vn2 = vn1 + K;
-  double* v = vn2 + K;               // current reflector rows i..M-1 (v[0] = 1)
-  double* rowi = v + K;              // A(i, offset..offset+k) with the trailing 1
-  int* piv = (int*)(rowi + PB + 1);
-  int* flag = piv + K;               // recompute flags
+  double* v = vn2 + K;               // reflector rows i..M-1 (v[0] = 1)
+  double* rowA = v + K;              // prefetched A(i, c) of the trailing columns
+  int* piv = (int*)(rowA + K);
+  int* flag = piv + K;
   __shared__ double red[NW];
   __shared__ double redv[NW];
   __shared__ int redi[NW];
   __shared__ double auxv[PB];
-  __shared__ int s_stop, s_rank, s_flagged;
+  __shared__ double rowi[PB + 1];
+  __shared__ int s_stop, s_rank, s_flagged, s_p;
 
   double* A = q.R0 + (int64_t)j * K * K;
   double* tau = q.tau + (int64_t)j * K;
@@ -107,37 +103,48 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
     while (k < nbp && !s_flagged) {
       const int i = offset + k;
       // ---- pivot: first max of vn1 over current positions i..N-1 ----
-      double bv = -1.0;
-      int bi = N;
-      for (int c = i + threadIdx.x; c < N; c += NT) {
-        const double x = vn1[c];
-        if (x > bv) {
-          bv = x;
-          bi = c;
+      {
+        double bv = -1.0;
+        int bi = N;
+        for (int c = i + threadIdx.x; c < N; c += NT) {
+          const double x = vn1[c];
+          if (x > bv) {
+            bv = x;
+            bi = c;
+          }
         }
-      }
-      argmax_lowest(bv, bi);
-      if (lane == 0) {
-        redv[wid] = bv;
-        redi[wid] = bi;
-      }
-      __syncthreads();
-      if (wid == 0) {
-        bv = lane < NW ? redv[lane] : -1.0;
-        bi = lane < NW ? redi[lane] : N;
         argmax_lowest(bv, bi);
-        if (lane == 0) redi[0] = bi;
+        if (lane == 0) {
+          redv[wid] = bv;
+          redi[wid] = bi;
+        }
+        __syncthreads();
+        if (wid == 0) {
+          bv = lane < NW ? redv[lane] : -1.0;
+          bi = lane < NW ? redi[lane] : N;
+          argmax_lowest(bv, bi);
+          if (lane == 0) s_p = bi;
+        }
+        __syncthreads();
+      }
+      const int p = s_p;
+      // ---- swap columns i <-> p fused with the pivot column's panel update:
+      //      v = A(i:M, p) - A(i:M, offset:i) F(p, 0:k)^T ----
+      double* ci = A + (int64_t)i * K;
+      double* cp = A + (int64_t)p * K;
+      for (int r = threadIdx.x; r < M; r += NT) {
+        const double xi = ci[r];
+        double xp = cp[r];
+        if (p != i) cp[r] = xi;
+        if (r < i) {
+          if (p != i) ci[r] = xp;
+        } else {
+          for (int kk = 0; kk < k; ++kk) xp -= A[(int64_t)(offset + kk) * K + r] * F[kk * K + p];
+          v[r - i] = xp;
+        }
       }
       __syncthreads();
-      const int p = redi[0];
       if (p != i) {
-        double* ci = A + (int64_t)i * K;
-        double* cp = A + (int64_t)p * K;
-        for (int r = threadIdx.x; r < M; r += NT) {
-          const double t = ci[r];
-          ci[r] = cp[r];
-          cp[r] = t;
-        }
         if (threadIdx.x < k) {
           const double t = F[threadIdx.x * K + i];
           F[threadIdx.x * K + i] = F[threadIdx.x * K + p];
@@ -154,20 +161,16 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
           flag[i] = f;
         }
       }
-      __syncthreads();
-      // ---- A(i:M, i) -= A(i:M, offset:i) F(i, 0:k)^T ; load into v ----
-      double* col = A + (int64_t)i * K;
-      for (int r = i + threadIdx.x; r < M; r += NT) {
-        double x = col[r];
-        for (int kk = 0; kk < k; ++kk) x -= A[(int64_t)(offset + kk) * K + r] * F[kk * K + i];
-        v[r - i] = x;
-      }
-      __syncthreads();
       // ---- dlarfg ----
       double ss = 0.0;
       for (int r = i + 1 + threadIdx.x; r < M; r += NT) ss += v[r - i] * v[r - i];
+      ss = fl::warp_sum(ss);
+      if (lane == 0) red[wid] = ss;
+      __syncthreads();
+      ss = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) ss += red[w];
       const double alpha = v[0];
-      ss = blk_sum(ss, red);
       const double xnorm = sqrt(ss);
       double beta, t;
       if (xnorm == 0.0) {
@@ -176,8 +179,6 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
       } else {
         beta = -copysign(hypot(alpha, xnorm), alpha);
         t = (beta - alpha) / beta;
-        const double scal = 1.0 / (alpha - beta);
-        for (int r = i + 1 + threadIdx.x; r < M; r += NT) v[r - i] *= scal;
       }
       if (i == 0) lead = fabs(beta);
       if (q.sigma > 0.0 && (lead == 0.0 || fabs(beta) < q.sigma * lead)) {
@@ -188,56 +189,92 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
         __syncthreads();
         break;
       }
+      {
+        const double scal = (xnorm == 0.0) ? 1.0 : 1.0 / (alpha - beta);
+        for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
+          const double x = v[r - i] * scal;
+          v[r - i] = x;
+          ci[r] = x;  // reflector below the diagonal
+        }
+      }
+      // prefetch row i of the trailing columns for the row update
+      for (int c = i + 1 + threadIdx.x; c < N; c += NT) rowA[c] = A[(int64_t)c * K + i];
       __syncthreads();
       if (threadIdx.x == 0) {
         v[0] = 1.0;
         tau[i] = t;
+        ci[i] = beta;
         q.diag[(int64_t)j * K + i] = fabs(beta);
       }
-      // write the reflector (below the diagonal) and R_ii = beta
-      for (int r = i + 1 + threadIdx.x; r < M; r += NT) col[r] = v[r - i];
-      if (threadIdx.x == 0) col[i] = beta;
       __syncthreads();
-      // ---- F(i+1:N, k) = t * A(i:M, i+1:N)^T v  (trailing columns, un-updated) ----
-      for (int c = i + 1 + wid; c < N; c += NW) {
-        const double* cc = A + (int64_t)c * K;
-        double d = 0.0;
-        for (int r = i + lane; r < M; r += 32) d += cc[r] * v[r - i];
-        d = fl::warp_sum(d);
-        if (lane == 0) F[k * K + c] = t * d;
-      }
-      // ---- auxv = -t * A(i:M, offset:i)^T v ----
-      for (int kk = wid; kk < k; kk += NW) {
-        const double* cc = A + (int64_t)(offset + kk) * K;
-        double d = 0.0;
-        for (int r = i + lane; r < M; r += 32) d += cc[r] * v[r - i];
-        d = fl::warp_sum(d);
-        if (lane == 0) auxv[kk] = -t * d;
+      // ---- F(i+1:N, k) = t A(i:M, i+1:N)^T v ; auxv = -t A(i:M, offset:i)^T v ----
+      {
+        const int ncol = N - i - 1;
+        // 16-byte loads: lane owns rows (2l, 2l+1) of each 64-row chunk, starting at
+        // the even row i0 <= i (row i-1 contributes v = 0); two chunks per trip
+        constexpr int CU = 8;  // columns in flight per warp
+        const int i0 = i & ~1;
+        for (int c0 = wid * CU; c0 < ncol; c0 += NW * CU) {
+          double d[CU];
+          const double* cc[CU];
+#pragma unroll
+          for (int u = 0; u < CU; ++u) {
+            d[u] = 0.0;
+            cc[u] = A + (int64_t)(i + 1 + min(c0 + u, ncol - 1)) * K;
+          }
+          for (int r = i0 + 2 * lane; r < M; r += 128) {
+            const int r2 = r + 64;
+            const double v0 = (r >= i) ? v[r - i] : 0.0;
+            const double v1 = (r + 1 < M) ? v[r + 1 - i] : 0.0;
+            const bool two = r2 < M;
+            const double w0 = two ? v[r2 - i] : 0.0;
+            const double w1 = (r2 + 1 < M) ? v[r2 + 1 - i] : 0.0;
+            double2 x[CU], y[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              x[u] = *reinterpret_cast<const double2*>(cc[u] + r);
+              y[u] = two ? *reinterpret_cast<const double2*>(cc[u] + r2) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
+          }
+#pragma unroll
+          for (int u = 0; u < CU; ++u) {
+            const double s = fl::warp_sum(d[u]);
+            if (lane == 0 && c0 + u < ncol) F[k * K + i + 1 + c0 + u] = t * s;
+          }
+        }
+        for (int kk = wid; kk < k; kk += NW) {
+          const double* cc = A + (int64_t)(offset + kk) * K;
+          double dd = 0.0;
+          for (int r = i + lane; r < M; r += 32) dd += cc[r] * v[r - i];
+          dd = fl::warp_sum(dd);
+          if (lane == 0) auxv[kk] = -t * dd;
+        }
+        if (threadIdx.x <= k)
+          rowi[threadIdx.x] = (threadIdx.x == k) ? 1.0 : A[(int64_t)(offset + threadIdx.x) * K + i];
       }
       __syncthreads();
-      // ---- F(:, k) += F(:, 0:k) auxv ; F(offset..i, k) = 0 ----
+      // ---- F(:, k) += F(:, 0:k) auxv (F(offset..i, k) = 0 first);
+      //      A(i, i+1:N) -= A(i, offset:i+1) F(i+1:N, 0:k+1)^T ; downdate ----
       for (int c = offset + threadIdx.x; c < N; c += NT) {
         double f = (c <= i) ? 0.0 : F[k * K + c];
         for (int kk = 0; kk < k; ++kk) f += F[kk * K + c] * auxv[kk];
         F[k * K + c] = f;
-      }
-      // row i of the panel columns: A(i, offset+kk) (reflector entries), 1 at k
-      if (threadIdx.x <= k) rowi[threadIdx.x] = (threadIdx.x == k) ? 1.0 : A[(int64_t)(offset + threadIdx.x) * K + i];
-      __syncthreads();
-      // ---- A(i, i+1:N) -= A(i, offset:i+1) F(i+1:N, 0:k+1)^T ; downdate ----
-      for (int c = i + 1 + threadIdx.x; c < N; c += NT) {
-        double x = A[(int64_t)c * K + i];
-        for (int kk = 0; kk <= k; ++kk) x -= rowi[kk] * F[kk * K + c];
-        A[(int64_t)c * K + i] = x;
-        if (i + 1 < M && vn1[c] != 0.0) {
-          double tt = fabs(x) / vn1[c];
-          tt = fmax(0.0, (1.0 + tt) * (1.0 - tt));
-          const double rr = vn1[c] / vn2[c];
-          if (tt * rr * rr <= tol3z) {
-            flag[c] = 1;
-            s_flagged = 1;
-          } else {
-            vn1[c] *= sqrt(tt);
+        if (c > i) {
+          double x = rowA[c];
+          for (int kk = 0; kk <= k; ++kk) x -= rowi[kk] * F[kk * K + c];
+          A[(int64_t)c * K + i] = x;
+          if (i + 1 < M && vn1[c] != 0.0) {
+            double tt = fabs(x) / vn1[c];
+            tt = fmax(0.0, (1.0 + tt) * (1.0 - tt));
+            const double rr = vn1[c] / vn2[c];
+            if (tt * rr * rr <= tol3z) {
+              flag[c] = 1;
+              s_flagged = 1;
+            } else {
+              vn1[c] *= sqrt(tt);
+            }
           }
         }
       }
@@ -246,36 +283,57 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
     }
     if (s_stop) break;
     const int kb = k;
-    const int rk = offset + kb;  // first row/col of the trailing block
+    const int rk = offset + kb;
     // ---- block update: A(rk:M, rk:N) -= A(rk:M, offset:rk) F(rk:N, 0:kb)^T  (DMMA) ----
     if (rk < M && rk < N) {
+      // warp = 8-row strip; the strip's panel fragments stay in registers and the
+      // 8-column tiles are software pipelined (next tile loaded before this one
+      // is stored) so the loop is not one memory round trip per tile
       const int g = lane >> 2, t4 = lane & 3;
       const int nrt = (M - rk + 7) / 8, nct = (N - rk + 7) / 8;
-      for (int tile = wid; tile < nrt * nct; tile += NW) {
-        const int r8 = rk + (tile % nrt) * 8, c8 = rk + (tile / nrt) * 8;
-        const int row = r8 + g, c0 = c8 + 2 * t4;
-        double d0 = (row < M && c0 < N) ? A[(int64_t)c0 * K + row] : 0.0;
-        double d1 = (row < M && c0 + 1 < N) ? A[(int64_t)(c0 + 1) * K + row] : 0.0;
-        for (int k0 = 0; k0 < kb; k0 += 4) {
-          const int kk = k0 + t4;
-          const double av = (row < M && kk < kb) ? -A[(int64_t)(offset + kk) * K + row] : 0.0;
-          const int cb = c8 + g;
-          const double bv = (cb < N && kk < kb) ? F[kk * K + cb] : 0.0;
-          fl::dmma(d0, d1, av, bv);
+      for (int rt = wid; rt < nrt; rt += NW) {
+        const int row = rk + rt * 8 + g;
+        const bool rok = row < M;
+        double av[PB / 4];
+#pragma unroll
+        for (int s = 0; s < PB / 4; ++s) {
+          const int kk = 4 * s + t4;
+          av[s] = (rok && kk < kb) ? -A[(int64_t)(offset + kk) * K + row] : 0.0;
         }
-        if (row < M && c0 < N) A[(int64_t)c0 * K + row] = d0;
-        if (row < M && c0 + 1 < N) A[(int64_t)(c0 + 1) * K + row] = d1;
+        auto ld = [&](int ct, double& x0, double& x1) {
+          const int c0 = rk + ct * 8 + 2 * t4;
+          x0 = (rok && c0 < N) ? A[(int64_t)c0 * K + row] : 0.0;
+          x1 = (rok && c0 + 1 < N) ? A[(int64_t)(c0 + 1) * K + row] : 0.0;
+        };
+        double d0, d1;
+        ld(0, d0, d1);
+        for (int ct = 0; ct < nct; ++ct) {
+          double n0 = 0.0, n1 = 0.0;
+          if (ct + 1 < nct) ld(ct + 1, n0, n1);
+          const int cb = rk + ct * 8 + g;
+#pragma unroll
+          for (int s = 0; s < PB / 4; ++s) {
+            const int kk = 4 * s + t4;
+            const double bv = (cb < N && kk < kb) ? F[kk * K + cb] : 0.0;
+            fl::dmma(d0, d1, av[s], bv);
+          }
+          const int c0 = rk + ct * 8 + 2 * t4;
+          if (rok && c0 < N) A[(int64_t)c0 * K + row] = d0;
+          if (rok && c0 + 1 < N) A[(int64_t)(c0 + 1) * K + row] = d1;
+          d0 = n0;
+          d1 = n1;
+        }
       }
     }
     __syncthreads();
     // ---- recompute flagged norms over rows rk..M-1 ----
     for (int c = rk + wid; c < N; c += NW) {
       if (!flag[c]) continue;
-      double ss = 0.0;
-      for (int r = rk + lane; r < M; r += 32) ss += A[(int64_t)c * K + r] * A[(int64_t)c * K + r];
-      ss = fl::warp_sum(ss);
+      double s2 = 0.0;
+      for (int r = rk + lane; r < M; r += 32) s2 += A[(int64_t)c * K + r] * A[(int64_t)c * K + r];
+      s2 = fl::warp_sum(s2);
       if (lane == 0) {
-        vn1[c] = vn2[c] = (rk < M) ? sqrt(ss) : 0.0;
+        vn1[c] = vn2[c] = (rk < M) ? sqrt(s2) : 0.0;
         flag[c] = 0;
       }
     }
@@ -286,13 +344,10 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
   const int rank = s_rank;
   for (int c = threadIdx.x; c < K; c += NT) {
     q.perm[(int64_t)j * K + c] = piv[c];
-    if (c >= rank) q.diag[(int64_t)j * K + c] = 0.0;
+    q.diag[(int64_t)j * K + c] =
+        (c < rank && lead > 0.0) ? q.diag[(int64_t)j * K + c] / lead : 0.0;
   }
-  __syncthreads();
   if (threadIdx.x == 0) q.rank[j] = rank;
-  // diag ratios |R_ii| / |R_00|
-  for (int c = threadIdx.x; c < rank; c += NT)
-    q.diag[(int64_t)j * K + c] = lead > 0.0 ? q.diag[(int64_t)j * K + c] / lead : 0.0;
 }
 
 }  // namespace
@@ -300,8 +355,8 @@ __global__ void __launch_bounds__(NT, 1) qrcp_kernel(QrcpArgs q) {
 namespace fl {
 int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
             int32_t* rank, double* diag, cudaStream_t s) {
-  const size_t smem = (size_t)(PB * K + 3 * K + PB + 1) * sizeof(double) + (size_t)2 * K * sizeof(int);
-  if (smem > 220 * 1024) return FL_ERR_INVALID;
+  const size_t smem = (size_t)(PB * K + 4 * K) * sizeof(double) + (size_t)2 * K * sizeof(int);
+  if (smem > 110 * 1024) return FL_ERR_INVALID;
   FL_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   QrcpArgs a{R0, K, kmax, sigma, tau, perm, rank, diag};
   qrcp_kernel<<<J, NT, smem, s>>>(a);

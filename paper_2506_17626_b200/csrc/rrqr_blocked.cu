@@ -142,6 +142,83 @@ __global__ void init_qhat_kernel(const double* __restrict__ Q1, int K, const int
   }
 }
 
+// Two consecutive 32-reflector panels (P0 = 64 q) -> one 64-wide compact WY:
+// T = [[T1, -T1 (V1^T V2) T2], [0, T2]] with V1 = columns P0..P0+31 (unit
+// diagonal from row P0), V2 = columns P0+32..P0+63 (unit diagonal from row
+// P0+32). X = V1^T V2 only involves rows >= P0+32 (V2 vanishes above).
+__global__ void __launch_bounds__(NT) combine_t_kernel(const double* __restrict__ W, const int64_t* __restrict__ off,
+                                                       const int32_t* __restrict__ ld,
+                                                       const int32_t* __restrict__ m, int K,
+                                                       const double* __restrict__ T32, double* __restrict__ T64,
+                                                       int q) {
+  constexpr int GC = 48, GLD = GC + 4;  // static smem <= 48 KB
+  __shared__ double V1s[NB * GLD];
+  __shared__ double V2s[NB * GLD];
+  __shared__ double Xs[NB * NB];
+  __shared__ double Ys[NB * NB];
+  const int j = blockIdx.y, P0 = 64 * q;
+  const int npan32 = K / NB, npan64 = K / 64;
+  const double* A = W + off[j];
+  const int64_t ldj = ld[j];
+  const int M = m[j] - (P0 + NB);  // rows of V2's support
+  const double* T1 = T32 + ((int64_t)j * npan32 + 2 * q) * NB * NB;
+  const double* T2 = T1 + NB * NB;
+  double* T = T64 + ((int64_t)j * npan64 + q) * 64 * 64;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  // X = V1^T V2: 16 tiles of 8x8, 2 per warp
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int r0 = 0; r0 < M; r0 += GC) {
+    for (int p = threadIdx.x; p < NB * GC; p += NT) {
+      const int col = p / GC, rr = p % GC, row = r0 + rr;  // row relative to P0 + 32
+      double v1 = 0.0, v2 = 0.0;
+      if (row < M) {
+        v1 = A[(int64_t)(P0 + col) * ldj + P0 + NB + row];  // below V1's diagonal block
+        if (row > col) v2 = A[(int64_t)(P0 + NB + col) * ldj + P0 + NB + row];
+        else if (row == col) v2 = 1.0;
+      }
+      V1s[col * GLD + rr] = v1;
+      V2s[col * GLD + rr] = v2;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int tile = 2 * w + u, ta = tile & 3, tb = tile >> 2;
+#pragma unroll 4
+      for (int k0 = 0; k0 < GC; k0 += 4)
+        fl::dmma(acc[u][0], acc[u][1], V1s[(ta * 8 + g) * GLD + k0 + t4], V2s[(tb * 8 + g) * GLD + k0 + t4]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int tile = 2 * w + u, ta = tile & 3, tb = tile >> 2;
+    Xs[(ta * 8 + g) * NB + tb * 8 + 2 * t4] = acc[u][0];
+    Xs[(ta * 8 + g) * NB + tb * 8 + 2 * t4 + 1] = acc[u][1];
+  }
+  __syncthreads();
+  // Y = X T2 (row-major Xs/Ys; T2 column-major: T2[b][c] at T2[c*NB + b])
+  for (int p = threadIdx.x; p < NB * NB; p += NT) {
+    const int a = p / NB, c = p % NB;
+    double s = 0.0;
+    for (int b = 0; b <= c; ++b) s += Xs[a * NB + b] * T2[c * NB + b];
+    Ys[a * NB + c] = s;
+  }
+  __syncthreads();
+  // T (column-major 64 x 64)
+  for (int p = threadIdx.x; p < 64 * 64; p += NT) {
+    const int c = p / 64, r = p % 64;
+    double val = 0.0;
+    if (r < NB && c < NB) val = T1[c * NB + r];
+    else if (r >= NB && c >= NB) val = T2[(c - NB) * NB + (r - NB)];
+    else if (r < NB && c >= NB) {
+      double s = 0.0;
+      for (int b = r; b < NB; ++b) s += T1[b * NB + r] * Ys[b * NB + (c - NB)];
+      val = -s;
+    }
+    T[p] = val;
+  }
+}
+
 // zero tau past the rank (reflectors that were never generated)
 __global__ void clamp_tau_kernel(double* tau, int K, const int32_t* rank) {
   const int j = blockIdx.x;
@@ -153,7 +230,7 @@ __global__ void clamp_tau_kernel(double* tau, int K, const int32_t* rank) {
 
 namespace {
 struct Workspace {
-  double *fac, *R0, *Q1, *T0, *T1, *tau0, *tau1;
+  double *fac, *R0, *Q1, *T0, *T1, *T64, *tau0, *tau1;
   int32_t* kmax;
 };
 
@@ -172,11 +249,35 @@ Workspace carve(void* base, int J, int K, int64_t store_elems, size_t* total) {
   ws.Q1 = (double*)take((size_t)J * K * K * 8);
   ws.T0 = (double*)take((size_t)J * npan * NB * NB * 8);
   ws.T1 = (double*)take((size_t)J * npan * NB * NB * 8);
+  ws.T64 = (double*)take((size_t)J * (K / 64 + 1) * 64 * 64 * 8);
   ws.tau0 = (double*)take((size_t)J * K * 8);
   ws.tau1 = (double*)take((size_t)J * K * 8);
   ws.kmax = (int32_t*)take((size_t)J * 4);
   if (total) *total = used;
   return ws;
+}
+
+// C_j[:, c_col0 : c_col0 + ncols] of the factor copy -= its own reflector panel at v_col0
+fl::WyArgs self_args(const fl_blockop* A, double* fac, int J, int v_col0, int c_col0, int ncols,
+                     const double* T, int64_t tstride, int transT) {
+  fl::WyArgs a{};
+  a.V = fac;
+  a.voff = A->off;
+  a.vld = A->ld;
+  a.C = fac;
+  a.coff = A->off;
+  a.cld = A->ld;
+  a.m = A->m;
+  a.T = T;
+  a.tstride = tstride;
+  a.v_col0 = v_col0;
+  a.c_col0 = c_col0;
+  a.row0 = v_col0;
+  a.transT = transT;
+  a.ncols_const = ncols;
+  a.tiles_per_block = (ncols + fl::wy_tn() - 1) / fl::wy_tn();
+  a.ntiles = J * a.tiles_per_block;
+  return a;
 }
 }  // namespace
 
@@ -195,44 +296,45 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
   cudaStream_t s = (cudaStream_t)stream;
   const int npan = K / NB;
   const int TN = fl::wy_tn();
+  const bool wide = (K % 64) == 0;  // 64-wide compact-WY updates
+  const int64_t t32s = (int64_t)npan * NB * NB, t64s = (int64_t)(K / 64) * 64 * 64;
   Workspace ws = carve(workspace, J, K, store_elems, nullptr);
   double* fac = ws.fac;
   // the raw blocks stay intact: factor a copy (same layout)
   FL_CUDA(cudaMemcpyAsync(fac, A->vals, (size_t)store_elems * 8, cudaMemcpyDeviceToDevice, s));
 
-  // ---- K2a: unpivoted blocked Householder QR, panels of NB columns ----
-  for (int p = 0; p < npan; ++p) {
-    const int P0 = p * NB;
-    int e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s);
-    if (e) return e;
-    const int ntrail = K - P0 - NB;
-    if (ntrail > 0) {
-      fl::WyArgs a{};
-      a.V = fac;
-      a.voff = A->off;
-      a.vld = A->ld;
-      a.C = fac;
-      a.coff = A->off;
-      a.cld = A->ld;
-      a.m = A->m;
-      a.T = ws.T0 + (int64_t)p * NB * NB;
-      a.tstride = (int64_t)npan * NB * NB;
-      a.v_col0 = P0;
-      a.c_col0 = P0 + NB;
-      a.row0 = P0;
-      a.transT = 1;
-      a.ncols_const = ntrail;
-      a.tiles_per_block = (ntrail + TN - 1) / TN;
-      a.ntiles = J * a.tiles_per_block;
-      e = fl::wy_apply(a, s);
-      if (e) return e;
+  // ---- K2a: unpivoted blocked Householder QR ----
+  int e;
+  if (wide) {
+    for (int q = 0; q < K / 64; ++q) {
+      const int P0 = 64 * q;
+      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s))) return e;
+      fl::WyArgs a = self_args(A, fac, J, P0, P0 + NB, NB, ws.T0 + (int64_t)(2 * q) * NB * NB, t32s, 1);
+      if ((e = fl::wy_apply_nb(a, 32, s))) return e;
+      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0 + NB, ws.tau0, ws.T0, s))) return e;
+      combine_t_kernel<<<dim3(1, J), NT, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.T0, ws.T64, q);
+      FL_CHECK_LAUNCH();
+      const int ntrail = K - P0 - 64;
+      if (ntrail > 0) {
+        a = self_args(A, fac, J, P0, P0 + 64, ntrail, ws.T64 + (int64_t)q * 64 * 64, t64s, 1);
+        if ((e = fl::wy_apply_nb(a, 64, s))) return e;
+      }
+    }
+  } else {
+    for (int p = 0; p < npan; ++p) {
+      const int P0 = p * NB;
+      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s))) return e;
+      const int ntrail = K - P0 - NB;
+      if (ntrail > 0) {
+        fl::WyArgs a = self_args(A, fac, J, P0, P0 + NB, ntrail, ws.T0 + (int64_t)p * NB * NB, t32s, 1);
+        if ((e = fl::wy_apply_nb(a, 32, s))) return e;
+      }
     }
   }
   // ---- K2b: truncated QRCP of R0 ----
   extract_r0_kernel<<<dim3(64, J), 256, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.R0, ws.kmax);
   FL_CHECK_LAUNCH();
-  int e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s);
-  if (e) return e;
+  if ((e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) return e;
   clamp_tau_kernel<<<J, 256, 0, s>>>(ws.tau1, K, rank);
   build_t_kernel<<<dim3(npan, J), NT, 0, s>>>(ws.R0, K, ws.kmax, ws.tau1, rank, ws.T1);
   init_q1_r_kernel<<<dim3(64, J), 256, 0, s>>>(ws.R0, K, rank, ws.Q1, R);
@@ -249,7 +351,7 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
     a.cld_const = K;
     a.m = ws.kmax;
     a.T = ws.T1 + (int64_t)p * NB * NB;
-    a.tstride = (int64_t)npan * NB * NB;
+    a.tstride = t32s;
     a.v_col0 = P0;
     a.c_col0 = P0;
     a.row0 = P0;
@@ -258,14 +360,14 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
     a.ncols_sub = P0;
     a.tiles_per_block = (K - P0 + TN - 1) / TN;
     a.ntiles = J * a.tiles_per_block;
-    e = fl::wy_apply(a, s);
-    if (e) return e;
+    if ((e = fl::wy_apply_nb(a, 32, s))) return e;
   }
-  // ---- K2c: Qhat = Q0 [Q1; 0], panels of Q0 in reverse ----
+  // ---- K2c: Qhat = Q0 [Q1; 0], reflector blocks of Q0 in reverse ----
   init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, (double*)Q->vals);
   FL_CHECK_LAUNCH();
-  for (int p = npan - 1; p >= 0; --p) {
-    const int P0 = p * NB;
+  const int wb = wide ? 64 : NB;
+  for (int p = K / wb - 1; p >= 0; --p) {
+    const int P0 = p * wb;
     fl::WyArgs a{};
     a.V = fac;
     a.voff = A->off;
@@ -274,8 +376,8 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
     a.coff = Q->off;
     a.cld = Q->ld;
     a.m = A->m;
-    a.T = ws.T0 + (int64_t)p * NB * NB;
-    a.tstride = (int64_t)npan * NB * NB;
+    a.T = wide ? ws.T64 + (int64_t)p * 64 * 64 : ws.T0 + (int64_t)p * NB * NB;
+    a.tstride = wide ? t64s : t32s;
     a.v_col0 = P0;
     a.c_col0 = 0;
     a.row0 = P0;
@@ -284,8 +386,7 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
     a.ncols_sub = 0;
     a.tiles_per_block = (K + TN - 1) / TN;
     a.ntiles = J * a.tiles_per_block;
-    e = fl::wy_apply(a, s);
-    if (e) return e;
+    if ((e = fl::wy_apply_nb(a, wb, s))) return e;
   }
   return FL_OK;
 }

@@ -1,17 +1,35 @@
 // Batched compact-WY block reflector application (see wy.cuh).
+//
+// Template NB in {32, 64} (reflectors per block), 8*NB/32 warps per CTA.
+// One CTA owns one (block, TN-column tile) and streams the rows in RC-row
+// chunks through a 3-stage cp.async pipeline, twice: phase 1 accumulates
+// W = V^T C (NB x TN) with the k (row) dimension split over two warp groups
+// (each warp: 2 x 4 mma tiles, 6 fragment loads per 8 DMMA), phase 2 forms
+// W' = op(T) W, phase 3 updates C -= V W' with W' held in registers and
+// writes each chunk back through shared memory with 16-byte stores.
+// NB = 64 doubles the arithmetic intensity per pass over C (4*NB flops per
+// 24 bytes), which moves the update from the HBM roof to the DMMA roof.
 #include "wy.cuh"
 
 namespace {
 
-constexpr int NB = 32;            // reflectors per panel
 constexpr int TN = 64;            // C columns per CTA
-constexpr int RC = 64;            // rows per staged chunk
-constexpr int NT = 256;           // 8 warps
-constexpr int LDS = RC + 4;       // padded column length of a staged chunk (conflict-free fragments)
+constexpr int RC = 32;            // rows per staged chunk
+constexpr int STAGES = 3;
+constexpr int LDS = RC + 4;       // padded column length of a staged chunk
 constexpr int LDW = TN + 4;       // padded row length of W
 
+template <int NB>
+struct Cfg {
+  static constexpr int NW = 8 * NB / 32;
+  static constexpr int NT = NW * 32;
+  static constexpr size_t smem = (size_t)(STAGES * NB * LDS + STAGES * TN * LDS + NB * LDW + NB * NB) * 8;
+};
+
+template <int NB>
 __device__ __forceinline__ void load_chunk(const double* __restrict__ V, int vld, const double* __restrict__ C,
                                            int cld, int ncol, int rbase, double* vs, double* cs) {
+  constexpr int NT = Cfg<NB>::NT;
   for (int p = threadIdx.x; p < NB * (RC / 2); p += NT) {
     const int col = p / (RC / 2), rr = (p % (RC / 2)) * 2, row = rbase + rr;
     double* dst = vs + col * LDS + rr;
@@ -24,23 +42,26 @@ __device__ __forceinline__ void load_chunk(const double* __restrict__ V, int vld
     if (col < ncol && row < cld) fl::cp_async16(dst, C + (int64_t)col * cld + row);
     else dst[0] = dst[1] = 0.0;
   }
-  fl::cp_async_commit();
 }
 
-// unit lower-trapezoidal mask of the first NB rows of V (chunk 0 only)
-__device__ __forceinline__ void mask_unit(double* vs) {
-  for (int p = threadIdx.x; p < NB * NB; p += NT) {
-    const int col = p / NB, row = p % NB;
-    if (row <= col) vs[col * LDS + row] = (row == col) ? 1.0 : 0.0;
+// unit lower-trapezoidal structure of V's first NB rows: chunk rows base..base+RC
+template <int NB>
+__device__ __forceinline__ void mask_unit(double* vs, int base) {
+  constexpr int NT = Cfg<NB>::NT;
+  for (int p = threadIdx.x; p < NB * RC; p += NT) {
+    const int col = p / RC, rr = p % RC, row = base + rr;
+    if (row <= col) vs[col * LDS + rr] = (row == col) ? 1.0 : 0.0;
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) wy_apply_kernel(fl::WyArgs a) {
+template <int NB>
+__global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kernel(fl::WyArgs a) {
+  constexpr int NW = Cfg<NB>::NW;
   extern __shared__ double sm[];
-  double* Vs = sm;                       // [2][NB][LDS]
-  double* Cs = Vs + 2 * NB * LDS;        // [2][TN][LDS]
-  double* Ws = Cs + 2 * TN * LDS;        // [NB][LDW]   W, then op(T) W
-  double* Ts = Ws + NB * LDW;            // [NB][NB]    column-major T
+  double* Vs = sm;                            // [STAGES][NB][LDS]
+  double* Cs = Vs + STAGES * NB * LDS;        // [STAGES][TN][LDS]
+  double* Ws = Cs + STAGES * TN * LDS;        // [NB][LDW]
+  double* Ts = Ws + NB * LDW;                 // [NB][NB] column-major
 
   int j, c0;
   if (a.tiles) {
@@ -60,138 +81,178 @@ __global__ void __launch_bounds__(NT, 1) wy_apply_kernel(fl::WyArgs a) {
   const int nchunks = (mj - r0 + RC - 1) / RC;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
-  for (int i = threadIdx.x; i < NB * NB; i += NT) Ts[i] = a.T[(int64_t)j * a.tstride + i];
+  for (int i = threadIdx.x; i < NB * NB; i += Cfg<NB>::NT) Ts[i] = a.T[(int64_t)j * a.tstride + i];
 
-  // ---------------- phase 1: W = V^T C  (W is NB x TN) ----------------
-  const int mt = w & 3, ntb = (w >> 2) * 4;
-  double acc[4][2];
+  auto stage_v = [&](int s) { return Vs + s * NB * LDS; };
+  auto stage_c = [&](int s) { return Cs + s * TN * LDS; };
+
+  // ---------------- phase 1: W = V^T C ----------------
+  constexpr int MB = NB / 16;  // m-tile pairs
+  const int kg = w / (NW / 2), wl = w % (NW / 2);
+  const int mb = wl % MB, nbk = wl / MB;
+  double acc[2][4][2];
 #pragma unroll
-  for (int n = 0; n < 4; ++n) acc[n][0] = acc[n][1] = 0.0;
-  load_chunk(V, vld, C, cld, ncol, r0, Vs, Cs);
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nchunks) load_chunk<NB>(V, vld, C, cld, ncol, r0 + s * RC, stage_v(s), stage_c(s));
+    fl::cp_async_commit();
+  }
   for (int ch = 0; ch < nchunks; ++ch) {
-    const int b = ch & 1;
-    if (ch + 1 < nchunks)
-      load_chunk(V, vld, C, cld, ncol, r0 + (ch + 1) * RC, Vs + (b ^ 1) * NB * LDS, Cs + (b ^ 1) * TN * LDS);
-    else
-      fl::cp_async_commit();
-    fl::cp_async_wait<1>();
+    const int nx = ch + STAGES - 1;
+    if (nx < nchunks)
+      load_chunk<NB>(V, vld, C, cld, ncol, r0 + nx * RC, stage_v(nx % STAGES), stage_c(nx % STAGES));
+    fl::cp_async_commit();
+    fl::cp_async_wait<STAGES - 1>();
     __syncthreads();
-    if (ch == 0) {
-      mask_unit(Vs);
+    if (ch * RC < NB) {
+      mask_unit<NB>(stage_v(ch % STAGES), ch * RC);
       __syncthreads();
     }
-    const double* vs = Vs + b * NB * LDS;
-    const double* cs = Cs + b * TN * LDS;
-#pragma unroll 4
-    for (int k0 = 0; k0 < RC; k0 += 4) {
-      const double av = vs[(mt * 8 + g) * LDS + k0 + t];
+    const double* vs = stage_v(ch % STAGES);
+    const double* cs = stage_c(ch % STAGES);
 #pragma unroll
-      for (int n = 0; n < 4; ++n) fl::dmma(acc[n][0], acc[n][1], av, cs[((ntb + n) * 8 + g) * LDS + k0 + t]);
+    for (int s = kg; s < RC / 4; s += 2) {
+      const int k0 = 4 * s;
+      double av[2], bv[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((2 * mb + mi) * 8 + g) * LDS + k0 + t];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bv[n] = cs[((4 * nbk + n) * 8 + g) * LDS + k0 + t];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) fl::dmma(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
     }
     __syncthreads();
   }
-#pragma unroll
-  for (int n = 0; n < 4; ++n) {
-    Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = acc[n][0];
-    Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = acc[n][1];
-  }
-  // prefetch the first chunk for phase 3 while phase 2 runs
-  load_chunk(V, vld, C, cld, ncol, r0, Vs, Cs);
-  __syncthreads();
-
-  // ---------------- phase 2: W <- op(T) W ----------------
-#pragma unroll
-  for (int n = 0; n < 4; ++n) acc[n][0] = acc[n][1] = 0.0;
-#pragma unroll
-  for (int k0 = 0; k0 < NB; k0 += 4) {
-    const int ar = mt * 8 + g, ac = k0 + t;
-    const double av = a.transT ? Ts[ar * NB + ac] : Ts[ac * NB + ar];  // op(T)[ar][ac]
-#pragma unroll
-    for (int n = 0; n < 4; ++n) fl::dmma(acc[n][0], acc[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int n = 0; n < 4; ++n) {
-    Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = acc[n][0];
-    Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = acc[n][1];
-  }
-  __syncthreads();
-
-  // ---------------- phase 3: C -= V W'  ----------------
-  // warp tile: rows 16*(w&3) .. +16 (two 8-row m-tiles), cols 32*(w>>2) .. +32
-  const int mrow = (w & 3) * 16, ncb = (w >> 2) * 4;
-  double bw[NB / 4][4];
-#pragma unroll
-  for (int k = 0; k < NB / 4; ++k)
-#pragma unroll
-    for (int n = 0; n < 4; ++n) bw[k][n] = Ws[(4 * k + t) * LDW + (ncb + n) * 8 + g];
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int b = ch & 1;
-    const int rbase = r0 + ch * RC;
-    if (ch + 1 < nchunks)
-      load_chunk(V, vld, C, cld, ncol, rbase + RC, Vs + (b ^ 1) * NB * LDS, Cs + (b ^ 1) * TN * LDS);
-    else
-      fl::cp_async_commit();
-    fl::cp_async_wait<1>();
-    __syncthreads();
-    if (ch == 0) {
-      mask_unit(Vs);
-      __syncthreads();
-    }
-    const double* vs = Vs + b * NB * LDS;
-    const double* cs = Cs + b * TN * LDS;
-    double c[2][4][2];
+  if (kg == 1) {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int n = 0; n < 4; ++n) {
-        const int row = mrow + mi * 8 + g, col = (ncb + n) * 8 + 2 * t;
-        c[mi][n][0] = cs[col * LDS + row];
-        c[mi][n][1] = cs[(col + 1) * LDS + row];
+        const int row = (2 * mb + mi) * 8 + g, col = (4 * nbk + n) * 8 + 2 * t;
+        Ws[row * LDW + col] = acc[mi][n][0];
+        Ws[row * LDW + col + 1] = acc[mi][n][1];
       }
+  }
 #pragma unroll
-    for (int k = 0; k < NB / 4; ++k) {
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nchunks) load_chunk<NB>(V, vld, C, cld, ncol, r0 + s * RC, stage_v(s), stage_c(s));
+    fl::cp_async_commit();
+  }
+  __syncthreads();
+  if (kg == 0) {
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const double av = -vs[(4 * k + t) * LDS + mrow + mi * 8 + g];
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int n = 0; n < 4; ++n) fl::dmma(c[mi][n][0], c[mi][n][1], av, bw[k][n]);
+      for (int n = 0; n < 4; ++n) {
+        const int row = (2 * mb + mi) * 8 + g, col = (4 * nbk + n) * 8 + 2 * t;
+        Ws[row * LDW + col] += acc[mi][n][0];
+        Ws[row * LDW + col + 1] += acc[mi][n][1];
       }
+  }
+  __syncthreads();
+
+  // ---------------- phase 2: W <- op(T) W  (NB x 64: 4 tiles per warp) ----------------
+  {
+    const int mt = w % (NB / 8), ntb = (w / (NB / 8)) * 4;
+    double p2[4][2];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) p2[n][0] = p2[n][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4) {
+      const int ar = mt * 8 + g, ac = k0 + t;
+      const double av = a.transT ? Ts[ar * NB + ac] : Ts[ac * NB + ar];  // op(T)[ar][ac]
+#pragma unroll
+      for (int n = 0; n < 4; ++n) fl::dmma(p2[n][0], p2[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
     }
+    __syncthreads();
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      const int row = rbase + mrow + mi * 8 + g;
-      if (row < mj) {
-#pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          const int col = (ncb + n) * 8 + 2 * t;
-          if (col < ncol) C[(int64_t)col * cld + row] = c[mi][n][0];
-          if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + row] = c[mi][n][1];
-        }
-      }
+    for (int n = 0; n < 4; ++n) {
+      Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = p2[n][0];
+      Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = p2[n][1];
     }
     __syncthreads();
   }
+
+  // ---------------- phase 3: C -= V W' ----------------
+  constexpr int NN = 32 / NW;  // n-tiles per warp: 4 (NB 32) or 2 (NB 64)
+  const int mrow = (w % 4) * 8, ncb = (w / 4) * NN;
+  double bw[NB / 4][NN];
+#pragma unroll
+  for (int k = 0; k < NB / 4; ++k)
+#pragma unroll
+    for (int n = 0; n < NN; ++n) bw[k][n] = Ws[(4 * k + t) * LDW + (ncb + n) * 8 + g];
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int nx = ch + STAGES - 1;
+    const int rbase = r0 + ch * RC;
+    if (nx < nchunks)
+      load_chunk<NB>(V, vld, C, cld, ncol, r0 + nx * RC, stage_v(nx % STAGES), stage_c(nx % STAGES));
+    fl::cp_async_commit();
+    fl::cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    if (ch * RC < NB) {
+      mask_unit<NB>(stage_v(ch % STAGES), ch * RC);
+      __syncthreads();
+    }
+    const double* vs = stage_v(ch % STAGES);
+    double* cs = stage_c(ch % STAGES);
+    double c[NN][2];
+#pragma unroll
+    for (int n = 0; n < NN; ++n) {
+      const int row = mrow + g, col = (ncb + n) * 8 + 2 * t;
+      c[n][0] = cs[col * LDS + row];
+      c[n][1] = cs[(col + 1) * LDS + row];
+    }
+#pragma unroll
+    for (int k = 0; k < NB / 4; ++k) {
+      const double av = -vs[(4 * k + t) * LDS + mrow + g];
+#pragma unroll
+      for (int n = 0; n < NN; ++n) fl::dmma(c[n][0], c[n][1], av, bw[k][n]);
+    }
+    // direct stores from the accumulators (no shared-memory round trip)
+    {
+      const int row = rbase + mrow + g;
+      if (row < mj) {
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          const int col = (ncb + n) * 8 + 2 * t;
+          if (col < ncol) C[(int64_t)col * cld + row] = c[n][0];
+          if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + row] = c[n][1];
+        }
+      }
+    }
+    __syncthreads();  // the stage is refilled by a later iteration's cp.async
+  }
+}
+
+template <int NB>
+int launch(const fl::WyArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA(cudaFuncSetAttribute(wy_apply_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Cfg<NB>::smem));
+    attr = true;
+  }
+  wy_apply_kernel<NB><<<a.ntiles, Cfg<NB>::NT, Cfg<NB>::smem, s>>>(a);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
 }
 
 }  // namespace
 
 namespace fl {
-size_t wy_smem_bytes() { return (size_t)(2 * NB * LDS + 2 * TN * LDS + NB * LDW + NB * NB) * sizeof(double); }
-
-int wy_apply(const WyArgs& a, cudaStream_t s) {
+int wy_apply(const WyArgs& a, cudaStream_t s) { return wy_apply_nb(a, 32, s); }
+int wy_apply_nb(const WyArgs& a, int nb, cudaStream_t s) {
   if (a.ntiles == 0) return FL_OK;
-  static bool attr = false;
-  if (!attr) {
-    FL_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)wy_smem_bytes()));
-    attr = true;
-  }
-  wy_apply_kernel<<<a.ntiles, NT, wy_smem_bytes(), s>>>(a);
-  FL_CHECK_LAUNCH();
-  return FL_OK;
+  if (nb == 64) return launch<64>(a, s);
+  if (nb == 32) return launch<32>(a, s);
+  return FL_ERR_INVALID;
 }
-int wy_nb() { return NB; }
+int wy_nb() { return 32; }
 int wy_tn() { return TN; }
 }  // namespace fl
 
@@ -199,7 +260,7 @@ int wy_tn() { return TN; }
 // caller-built tables (all device pointers), for kernel-level tests.
 extern "C" int fl_dev_wy_apply(const double* V, const int64_t* voff, const int32_t* vld, double* C,
                                const int64_t* coff, const int32_t* cld, const int32_t* m, const double* T,
-                               int64_t tstride, int32_t row0, int32_t transT, const int32_t* ncols,
+                               int64_t tstride, int32_t nb, int32_t row0, int32_t transT, const int32_t* ncols,
                                const int32_t* tiles, int32_t ntiles, void* stream) {
   fl::WyArgs a{};
   a.V = V;
@@ -211,13 +272,10 @@ extern "C" int fl_dev_wy_apply(const double* V, const int64_t* voff, const int32
   a.m = m;
   a.T = T;
   a.tstride = tstride;
-  a.v_col0 = 0;
-  a.c_col0 = 0;
   a.row0 = row0;
   a.transT = transT;
   a.ncols = ncols;
-  a.ncols_sub = 0;
   a.tiles = tiles;
   a.ntiles = ntiles;
-  return fl::wy_apply(a, (cudaStream_t)stream);
+  return fl::wy_apply_nb(a, nb, (cudaStream_t)stream);
 }

@@ -41,6 +41,9 @@ struct WyArgs {
   int32_t ntiles;
 };
 
+int wy_apply(const WyArgs& a, cudaStream_t s);               // NB = 32
+int wy_apply_nb(const WyArgs& a, int nb, cudaStream_t s);    // NB = 32 or 64
+
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)

@@ -30,13 +30,13 @@ def _blocks(ms, ncols, ld_align=16, rng=None):
     return buf, offs, np.array(lds, np.int32), mats
 
 
+@pytest.mark.parametrize("NB", [32, 64])
 @pytest.mark.parametrize("transT", [0, 1])
 @pytest.mark.parametrize("row0", [0, 32])
-def test_wy_apply_matches_numpy(dev, transT, row0):
+def test_wy_apply_matches_numpy(dev, transT, row0, NB):
     torch, D, _lib = dev
-    rng = np.random.default_rng(3 + transT + row0)
-    NB = 32
-    ms = [row0 + 40, row0 + 257, row0 + 64, row0 + 1000]
+    rng = np.random.default_rng(3 + transT + row0 + NB)
+    ms = [row0 + NB + 8, row0 + 257, row0 + NB, row0 + 1000]
     ncol = 150
     vbuf, voff, vld, vmats = _blocks(ms, NB, rng=rng)
     cbuf, coff, cld, cmats = _blocks(ms, ncol, rng=rng)
@@ -48,7 +48,7 @@ def test_wy_apply_matches_numpy(dev, transT, row0):
         ncols=np.full(len(ms), ncol, np.int32), tiles=tiles.ravel()).items()}
     _lib.check(_lib.lib().fl_dev_wy_apply(
         D.ptr(d["V"]), D.ptr(d["voff"]), D.ptr(d["vld"]), D.ptr(d["C"]), D.ptr(d["coff"]),
-        D.ptr(d["cld"]), D.ptr(d["m"]), D.ptr(d["T"]), NB * NB, row0, transT, D.ptr(d["ncols"]),
+        D.ptr(d["cld"]), D.ptr(d["m"]), D.ptr(d["T"]), NB * NB, NB, row0, transT, D.ptr(d["ncols"]),
         D.ptr(d["tiles"]), len(tiles), D.stream_ptr()), "wy")
     out = d["C"].cpu().numpy()
     for j, m in enumerate(ms):
