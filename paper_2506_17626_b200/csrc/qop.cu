@@ -22,8 +22,16 @@
 // column-oriented back substitution against R_j, scatter to kept columns.
 #include <float.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
+
+namespace fl {
+bool fused_ok(const fl_blockop* op);
+int lsqr_fused_init(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, cudaStream_t s);
+int lsqr_fused_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t first_it,
+                       int64_t count, cudaStream_t s);
+}  // namespace fl
 
 namespace {
 
@@ -427,6 +435,13 @@ int set_smem(const void* fn, size_t bytes) {
 size_t col_smem(const fl_blockop* op) { return (size_t)(op->max_ncols > 0 ? op->max_ncols : 1) * sizeof(double); }
 size_t row_smem(const fl_blockop* op) { return (size_t)(op->max_rows > 0 ? op->max_rows : 1) * sizeof(double); }
 int grid_rows(const fl_blockop* op) { return (op->nrows + NT - 1) / NT; }
+// one HBM pass per iteration (lsqr_fused.cu) unless a column tile does not fit
+// on chip or FEATLSQ_LSQR=split asks for the two-pass kernels
+bool use_fused(const fl_blockop* op) {
+  const char* e = getenv("FEATLSQ_LSQR");
+  if (e && e[0] == 's') return false;
+  return fl::fused_ok(op);
+}
 }  // namespace
 
 extern "C" int fl_blockop_apply(const fl_blockop* op, const double* x, double* out, void* stream) {
@@ -459,6 +474,7 @@ extern "C" int fl_lsqr_init(const fl_blockop* op, const double* rhs, fl_lsqr_vec
   lsqr_init_a<<<grid_rows(op), NT, 0, s>>>(*op, rhs, *vecs, st);
   FL_CHECK_LAUNCH();
   if (op->n_col_tiles == 0) return FL_OK;
+  if (use_fused(op)) return fl::lsqr_fused_init(op, vecs, st, s);
   int e = set_smem((const void*)lsqr_init_b, row_smem(op));
   if (e) return e;
   lsqr_init_b<<<op->n_col_tiles, NT, row_smem(op), s>>>(*op, *vecs, st);
@@ -470,6 +486,7 @@ extern "C" int fl_lsqr_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr
                                int64_t count, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (op->n_col_tiles == 0 || op->n_row_tiles == 0) return FL_ERR_INVALID;
+  if (use_fused(op)) return fl::lsqr_fused_iterate(op, vecs, st, first_it, count, s);
   int e = set_smem((const void*)lsqr_qv_kernel, col_smem(op));
   if (e) return e;
   e = set_smem((const void*)lsqr_qtu_kernel, row_smem(op));
