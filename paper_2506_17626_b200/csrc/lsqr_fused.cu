@@ -49,8 +49,7 @@ __global__ void __launch_bounds__(NT, 1) fused_kernel(fl_blockop op, fl_lsqr_vec
   if (is_done(st)) return;
   extern __shared__ double sm[];
   double* tile = sm;               // [STAGES][W][ldmax] column tiles of Q_j
-  __shared__ double red[NW * W];
-  __shared__ double tcol[W];
+  __shared__ double red[2 * NW * W];
   __shared__ double red2[NW];
   __shared__ __align__(8) uint64_t bars[STAGES];
   __shared__ double vsh[VMAX];  // v_j, staged once (off the reduction's critical path)
@@ -164,30 +163,37 @@ __global__ void __launch_bounds__(NT, 1) fused_kernel(fl_blockop op, fl_lsqr_vec
 #pragma unroll
       for (int c = 0; c < W; ++c) {
         const double s = fl::warp_sum(acc[c]);
-        if (lane == 0) red[wid * W + c] = s;
+        if (lane == 0) red[(tdx & 1) * NW * W + wid * W + c] = s;
       }
       __syncthreads();  // partials visible; every thread is done with tile tdx-1
       issue(tdx + STAGES - 1);  // refills the stage tile tdx-1 used
-      if (wid == 0) {
-        // v'[tile] = Q[:, tile]^T u - beta v[tile] (solvers.py:136), fixed-order sum
+      // v'[tile] = Q[:, tile]^T u - beta v[tile] (solvers.py:136): every warp
+      // sums the NW warp partials itself with the same 16-lane shuffle tree
+      // (two columns per pass: lanes 0-15 column c, lanes 16-31 column c+1),
+      // so no second barrier is needed; `red` alternates buffers by tile parity
+      double tc[W];
+      const double* rb = red + (tdx & 1) * NW * W;
 #pragma unroll
-        for (int c = 0; c < W; ++c) {
-          double s = (lane < NW) ? red[lane * W + c] : 0.0;
-          s = fl::warp_sum(s);
-          const int col = tdx * W + c;
-          double vn = 0.0;
-          if (c < ncl) vn = s - ((mode == 1) ? beta * vsh[col] : 0.0);
-          if (lane == 0) {
-            tcol[c] = vn;
-            if (c < ncl) vec.vp[co + col] = vn;
-            ass += vn * vn;
-          }
+      for (int c0 = 0; c0 < W; c0 += 2) {
+        const int c = c0 + (lane >> 4);
+        double s = (c < W) ? rb[(lane & 15) * W + c] : 0.0;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double s0 = __shfl_sync(0xffffffffu, s, 0), s1 = __shfl_sync(0xffffffffu, s, 16);
+        tc[c0] = s0;
+        if (c0 + 1 < W) tc[c0 + 1] = s1;
+      }
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        const int col = tdx * W + c;
+        double vn = 0.0;
+        if (c < ncl) vn = tc[c] - ((mode == 1) ? beta * vsh[col] : 0.0);
+        tc[c] = vn;
+        if (threadIdx.x == 0) {
+          if (c < ncl) vec.vp[co + col] = vn;
+          ass += vn * vn;
         }
       }
-      __syncthreads();
-      double tc[W];
-#pragma unroll
-      for (int c = 0; c < W; ++c) tc[c] = tcol[c];
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int r = threadIdx.x + i * NT;
