@@ -137,6 +137,26 @@ def fp64_peak(torch, D, _lib):
 
 
 # ---------------------------------------------------------------- work counts
+def launches_per_step(fs, iters):
+    """Kernels of this library launched per solve (rrqr_blocked.cu / qop.cu /
+    lsqr_fused.cu launch sequences)."""
+    from paper_2506_17626_b200.filtering import rrqr_route
+    K = fs.K
+    if rrqr_route(fs.qstore.layout) == "blocked":
+        npan = K // 32
+        if K % 64 == 0:
+            q = K // 64
+            k2a = 4 * q + (q - 1)            # panel, wy32, panel, combine_t, wy64
+            k2c = q
+        else:
+            k2a = npan + (npan - 1)
+            k2c = npan
+        rrqr = k2a + 5 + npan + 1 + k2c      # extract, qrcp, clamp, build_t, init_q1_r, Q1, init_qhat
+    else:
+        rrqr = 1
+    return 1 + rrqr + 2 + 2 * iters + 1      # assemble, rrqr, lsqr init, iterations, recover
+
+
 def rrqr_flops(m, K, r):
     """F_alg (truncated QRCP + thin Q + initial norms) and
     F_ref (full dgeqp3 + dorgqr, what the reference executes)."""
@@ -228,7 +248,11 @@ def product(args, rank, world, local_rank):
     nnz_q = int(np.sum(m * fs.ranks))
     nnz_a = int(m.sum()) * L.K
     f_alg, f_ref = rrqr_flops(m, L.K, fs.ranks)
-    bytes_it = 8.0 * (2 * nnz_q + 2 * L.nrows + 6 * fs.kept_total)
+    # compulsory bytes of one fused iteration: Q read once (the kernel reuses
+    # each staged column tile for Q^T u and Q v'), u/partials, 6 y-space vectors
+    bytes_it = 8.0 * (nnz_q + 2 * L.partial_len + 2 * L.nrows + 6 * fs.kept_total)
+    # SURVEY.md §8(d) per-iteration bytes assume two passes over Q (Q v, Q^T u)
+    bytes_survey = 8.0 * (2 * nnz_q + 2 * L.nrows + 6 * fs.kept_total)
     t_it = t_lsqr / iters
     hbm, hbm_src = peaks()
     fp64 = fp64_peak(torch, D, _lib)
@@ -252,7 +276,7 @@ def product(args, rank, world, local_rank):
                    "rows": L.nrows, "cols": int(L.J * L.K), "kept": int(fs.kept_total),
                    "l2": f"inputs larger than L2 (Q {nnz_q * 8 / 1e9:.2f} GB, A {nnz_a * 8 / 1e9:.2f} GB)",
                    "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm", "kernel": "LSQR iteration (qv + ured + qtu)",
+        "roofline": {"bound": "hbm", "kernel": "LSQR iteration (fused_kernel + row_kernel)",
                      "achieved": round(bytes_it / t_it / 1e9, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(bytes_it / t_it / 1e9 / hbm, 4),
                      "traffic": traffic, "peak_source": hbm_src,
@@ -267,13 +291,15 @@ def product(args, rank, world, local_rank):
                                     "frac_fp64_peak": round(f_alg / t_rrqr / 1e12 / fp64_peak_tf, 4),
                                     "fp64_peak_TF_measured": fp64},
             "lsqr": {"ms_per_iter": round(t_it * 1e3, 4), "GB/s": round(bytes_it / t_it / 1e9, 1),
-                     "frac_hbm": round(bytes_it / t_it / 1e9 / hbm, 4), "init_ms": round(t_init * 1e3, 3),
+                     "frac_hbm": round(bytes_it / t_it / 1e9 / hbm, 4),
+                     "GB/s_survey_two_pass_bytes": round(bytes_survey / t_it / 1e9, 1),
+                     "init_ms": round(t_init * 1e3, 3),
                      "phibar": st.phibar, "iterations": int(st.it)},
             "recover": {"ms": round(t_rec * 1e3, 3)},
             "solve_s": round(step_s, 4),
         },
         "clocks": clk,
-        "gpu_launches": args.steps * (1 + 1 + 2 + 3 * iters + 1),
+        "gpu_launches": args.steps * launches_per_step(fs, iters),
     }
 
     # ---- end to end through the public API, host buffers
