@@ -82,6 +82,7 @@ typedef struct fl_blockop {
   double* partial;          /* (partial_len,) scratch */
   double* red_scratch;      /* (>= max(n_row_tiles, n_col_tiles) + 64) scratch */
   unsigned int* counter;    /* (4,) zero-initialised scratch */
+  const int32_t* order;     /* (J,) block processing order (largest first), NULL = 0..J-1 */
 } fl_blockop;
 
 #define FL_ROW_TILE 256

@@ -152,8 +152,11 @@ class DeviceBlocks:
             t = torch()
             L = self.layout
             n_scr = 2 * max(len(self.col_tiles), len(L.row_tiles), (L.nrows + 255) // 256, 1) + 64
+            # largest blocks first: the per-block LSQR CTAs then finish with a short tail
+            work = L.m.astype(np.int64) * np.maximum(self.ncols.astype(np.int64), 1)
+            order = np.argsort(-work, kind="stable").astype(np.int32)
             self._dev = dict(ncols=to_dev(self.ncols), col_off=to_dev(self.col_off),
-                             col_tiles=to_dev(self.col_tiles),
+                             col_tiles=to_dev(self.col_tiles), order=to_dev(order),
                              scratch=t.zeros(n_scr, dtype=t.float64, device=require_cuda()))
         return self._dev
 
@@ -170,7 +173,7 @@ class DeviceBlocks:
                 n_row_tiles=len(L.row_tiles), row_tiles=ptr(Ld["row_tiles"]),
                 n_col_tiles=len(self.col_tiles), col_tiles=ptr(d["col_tiles"]),
                 partial=ptr(Ld["partial"]), red_scratch=ptr(d["scratch"]),
-                counter=ptr(Ld["counter"]))
+                counter=ptr(Ld["counter"]), order=ptr(d["order"]))
         return self._struct
 
     # ---- products (stream ordered; results stay on device) ----

@@ -34,6 +34,7 @@ class BlockOp(C.Structure):
         ("n_row_tiles", C.c_int32), ("row_tiles", C.c_void_p),
         ("n_col_tiles", C.c_int32), ("col_tiles", C.c_void_p),
         ("partial", C.c_void_p), ("red_scratch", C.c_void_p), ("counter", C.c_void_p),
+        ("order", C.c_void_p),
     ]
 
 

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(NT, 1) fused_kernel(fl_blockop op, fl_lsqr_vec
   }
   __syncthreads();
 
-  const int j = blockIdx.x;
+  const int j = op.order ? op.order[blockIdx.x] : blockIdx.x;  // largest blocks first (shorter tail)
   const int m = op.m[j];
   const int ld = op.ld[j];
   const int nc = op.ncols[j];

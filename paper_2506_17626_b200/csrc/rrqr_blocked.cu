@@ -11,6 +11,7 @@
 // per-block size that depends on the rank is read by the kernels from device
 // memory (tiles past r_j exit immediately).
 #include <float.h>
+#include <stdlib.h>
 
 #include "wy.cuh"
 
@@ -287,21 +288,16 @@ extern "C" int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t
   return (int64_t)total;
 }
 
-extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
-                               double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,
-                               void* workspace, void* stream) {
-  if (!(sigma >= 0.0 && sigma < 1.0) || K < NB || K % NB) return FL_ERR_INVALID;
-  const int J = A->nblocks;
-  if (J == 0) return FL_OK;
-  cudaStream_t s = (cudaStream_t)stream;
+namespace {
+// The whole route for the J blocks of one group; A, Q, R, perm, rank, diag
+// and the workspace arrays are already offset to the group's first block.
+int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, double* R, int32_t* perm,
+              int32_t* rank, double* diag, const Workspace& ws, int J, cudaStream_t s, cudaEvent_t k2a_done) {
   const int npan = K / NB;
   const int TN = fl::wy_tn();
   const bool wide = (K % 64) == 0;  // 64-wide compact-WY updates
   const int64_t t32s = (int64_t)npan * NB * NB, t64s = (int64_t)(K / 64) * 64 * 64;
-  Workspace ws = carve(workspace, J, K, store_elems, nullptr);
   double* fac = ws.fac;
-  // the raw blocks stay intact: factor a copy (same layout)
-  FL_CUDA(cudaMemcpyAsync(fac, A->vals, (size_t)store_elems * 8, cudaMemcpyDeviceToDevice, s));
 
   // ---- K2a: unpivoted blocked Householder QR ----
   int e;
@@ -331,6 +327,7 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
       }
     }
   }
+  if (k2a_done) FL_CUDA(cudaEventRecord(k2a_done, s));
   // ---- K2b: truncated QRCP of R0 ----
   extract_r0_kernel<<<dim3(64, J), 256, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.R0, ws.kmax);
   FL_CHECK_LAUNCH();
@@ -389,4 +386,76 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
     if ((e = fl::wy_apply_nb(a, wb, s))) return e;
   }
   return FL_OK;
+}
+
+constexpr int MAX_GROUPS = 8;
+cudaStream_t g_streams[MAX_GROUPS] = {};
+
+int group_count(int J) {
+  const char* e = getenv("FEATLSQ_RRQR_GROUPS");
+  int g = e ? atoi(e) : 4;
+  if (g < 1) g = 1;
+  if (g > MAX_GROUPS) g = MAX_GROUPS;
+  while (g > 1 && J / g < 32) --g;  // keep every group a full wave of blocks
+  return g;
+}
+}  // namespace
+
+// Blocks are split into G groups, each run through the whole route on its own
+// stream, group g+1 starting when group g has finished K2a: the latency- and
+// HBM-bound K2b of one group overlaps the DMMA-bound K2a/K2c of the others.
+extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
+                               double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,
+                               void* workspace, void* stream) {
+  if (!(sigma >= 0.0 && sigma < 1.0) || K < NB || K % NB) return FL_ERR_INVALID;
+  const int J = A->nblocks;
+  if (J == 0) return FL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  Workspace ws = carve(workspace, J, K, store_elems, nullptr);
+  // the raw blocks stay intact: factor a copy (same layout, absolute offsets)
+  FL_CUDA(cudaMemcpyAsync(ws.fac, A->vals, (size_t)store_elems * 8, cudaMemcpyDeviceToDevice, s));
+  const int G = group_count(J);
+  if (G == 1) return run_group(A, Q, K, sigma, R, perm, rank, diag, ws, J, s, nullptr);
+
+  const int64_t kk = (int64_t)K * K, t32s = (int64_t)(K / NB) * NB * NB, t64s = (int64_t)(K / 64) * 64 * 64;
+  cudaEvent_t start, k2a[MAX_GROUPS], done[MAX_GROUPS];
+  FL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  FL_CUDA(cudaEventRecord(start, s));
+  int err = FL_OK;
+  for (int g = 0; g < G && !err; ++g) {
+    if (!g_streams[g]) FL_CUDA(cudaStreamCreateWithFlags(&g_streams[g], cudaStreamNonBlocking));
+    FL_CUDA(cudaEventCreateWithFlags(&k2a[g], cudaEventDisableTiming));
+    FL_CUDA(cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming));
+    const int j0 = (int)((int64_t)J * g / G), j1 = (int)((int64_t)J * (g + 1) / G), Jg = j1 - j0;
+    cudaStream_t sg = g_streams[g];
+    FL_CUDA(cudaStreamWaitEvent(sg, start, 0));
+    if (g > 0) FL_CUDA(cudaStreamWaitEvent(sg, k2a[g - 1], 0));
+    fl_blockop Ag = *A, Qg = *Q;
+    Ag.nblocks = Qg.nblocks = Jg;
+    Ag.off += j0;
+    Ag.ld += j0;
+    Ag.m += j0;
+    Qg.off += j0;
+    Qg.ld += j0;
+    Qg.m += j0;
+    Workspace wg = ws;
+    wg.R0 += j0 * kk;
+    wg.Q1 += j0 * kk;
+    wg.T0 += j0 * t32s;
+    wg.T1 += j0 * t32s;
+    wg.T64 += j0 * t64s;
+    wg.tau0 += (int64_t)j0 * K;
+    wg.tau1 += (int64_t)j0 * K;
+    wg.kmax += j0;
+    err = run_group(&Ag, &Qg, K, sigma, R + j0 * kk, perm + (int64_t)j0 * K, rank + j0, diag + (int64_t)j0 * K,
+                    wg, Jg, sg, k2a[g]);
+    FL_CUDA(cudaEventRecord(done[g], sg));
+    FL_CUDA(cudaStreamWaitEvent(s, done[g], 0));
+  }
+  cudaEventDestroy(start);
+  for (int g = 0; g < G; ++g) {
+    cudaEventDestroy(k2a[g]);
+    cudaEventDestroy(done[g]);
+  }
+  return err;
 }
