@@ -71,6 +71,25 @@ def round_up(x, a):
     return (x + a - 1) // a * a
 
 
+def tile_table(extent, step) -> np.ndarray:
+    """(n, 2) int32 rows (j, start) for start in range(0, extent[j], step)."""
+    extent = np.asarray(extent, dtype=np.int64)
+    per = (extent + step - 1) // step
+    j = np.repeat(np.arange(extent.size, dtype=np.int64), per)
+    first = np.repeat(np.cumsum(per) - per, per)
+    start = (np.arange(j.size, dtype=np.int64) - first) * step
+    return np.stack([j, start], axis=1).astype(np.int32).reshape(-1, 2)
+
+
+def stable_argsort(keys: np.ndarray) -> np.ndarray:
+    """Stable argsort as int32 (on the device when one is present)."""
+    t = torch()
+    if keys.size > 1 << 16 and t.cuda.is_available():
+        k = t.from_numpy(np.ascontiguousarray(keys)).to(require_cuda())
+        return t.sort(k, stable=True).indices.to(t.int32).cpu().numpy()
+    return np.argsort(keys, kind="stable").astype(np.int32)
+
+
 class BlockLayout:
     """Row structure of a block store (see module docstring)."""
 
@@ -92,15 +111,13 @@ class BlockLayout:
                      else np.zeros(0, np.int32))
         # gather map: sources of each global row in increasing partial index
         # (= increasing block index, as blocks are concatenated in order)
-        order = np.argsort(self.rows, kind="stable").astype(np.int32)
+        self.gsrc = stable_argsort(self.rows)
         counts = np.bincount(self.rows, minlength=self.nrows) if self.rows.size else \
             np.zeros(self.nrows, np.int64)
         self.gptr = np.zeros(self.nrows + 1, dtype=np.int32)
         self.gptr[1:] = np.cumsum(counts)
-        self.gsrc = order
         # forward (row) tiles: one CTA per FL_ROW_TILE rows of a block
-        tiles = [(j, r0) for j in range(self.J) for r0 in range(0, int(self.m[j]), _lib.FL_ROW_TILE)]
-        self.row_tiles = np.array(tiles, dtype=np.int32).reshape(-1, 2)
+        self.row_tiles = tile_table(self.m, _lib.FL_ROW_TILE)
         self.max_rows = int(self.m.max()) if self.J else 0
         self._dev = None
 
@@ -142,8 +159,7 @@ class DeviceBlocks:
         self.ncols = np.asarray(ncols, dtype=np.int32)
         self.col_off = np.asarray(col_off, dtype=np.int64)
         self.ncols_total = int((self.col_off + self.ncols).max()) if layout.J else 0
-        tiles = [(j, c0) for j in range(layout.J) for c0 in range(0, int(self.ncols[j]), _lib.FL_COL_TILE)]
-        self.col_tiles = np.array(tiles, dtype=np.int32).reshape(-1, 2)
+        self.col_tiles = tile_table(self.ncols, _lib.FL_COL_TILE)
         self._dev = None
         self._struct = None
 

@@ -232,9 +232,7 @@ class AssemblyPlan:
         self.rows_per_block = rows_per_block
         self.problem, self.dec, self.basis = problem, dec, basis
         self.axes, self.n_interior, self.row_count = axes, n_interior, row_count
-        tiles = np.array([(j, r0) for j in range(J) for r0 in range(0, int(self.layout.ld[j]),
-                                                                      _lib.FL_ASM_TILE)],
-                         dtype=np.int32).reshape(-1, 2)
+        tiles = D.tile_table(self.layout.ld, _lib.FL_ASM_TILE)
         self.keep = keep = dict(
             centers=D.to_dev(np.asarray(dec.centers, float)),
             half=D.to_dev(np.asarray(dec.half_widths, float)),
