@@ -79,14 +79,17 @@ typedef struct fl_blockop {
   const int32_t* row_tiles; /* (n_row_tiles, 2): block, first row */
   int32_t n_col_tiles;      /* tiles of FL_COL_TILE columns */
   const int32_t* col_tiles; /* (n_col_tiles, 2): block, first column */
-  double* partial;          /* (partial_len,) scratch */
-  double* red_scratch;      /* (>= max(n_row_tiles, n_col_tiles) + 64) scratch */
+  double* partial;          /* (FL_LSQR_SPLIT_MAX * partial_len,) scratch */
+  double* red_scratch;      /* (>= 2 * max(n_row_tiles, n_col_tiles, FL_LSQR_SPLIT_MAX * J) + 64) scratch */
   unsigned int* counter;    /* (4,) zero-initialised scratch */
   const int32_t* order;     /* (J,) block processing order (largest first), NULL = 0..J-1 */
 } fl_blockop;
 
 #define FL_ROW_TILE 256
 #define FL_COL_TILE 32
+/* The fused LSQR iteration may split each block's columns over up to this
+ * many CTAs (each writes its own copy of the block's partial product). */
+#define FL_LSQR_SPLIT_MAX 4
 
 /* ------------------------------------------------------------------------
  * Assembly (assembly.py:124-238). Row r of block j: r < prod(box_cnt) is the

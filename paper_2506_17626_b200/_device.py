@@ -128,7 +128,8 @@ class BlockLayout:
                 off=to_dev(self.off), ld=to_dev(self.ld), m=to_dev(self.m),
                 row_off=to_dev(self.row_off), rows=to_dev(self.rows), gptr=to_dev(self.gptr),
                 gsrc=to_dev(self.gsrc), row_tiles=to_dev(self.row_tiles),
-                partial=t.empty(max(self.partial_len, 1), dtype=t.float64, device=require_cuda()),
+                partial=t.empty(max(_lib.FL_LSQR_SPLIT_MAX * self.partial_len, 1), dtype=t.float64,
+                                device=require_cuda()),
                 counter=t.zeros(4, dtype=t.int32, device=require_cuda()),
             )
         return self._dev
@@ -167,7 +168,8 @@ class DeviceBlocks:
         if self._dev is None:
             t = torch()
             L = self.layout
-            n_scr = 2 * max(len(self.col_tiles), len(L.row_tiles), (L.nrows + 255) // 256, 1) + 64
+            n_scr = 2 * max(len(self.col_tiles), len(L.row_tiles), (L.nrows + 255) // 256,
+                            _lib.FL_LSQR_SPLIT_MAX * L.J, 1) + 64
             # largest blocks first: the per-block LSQR CTAs then finish with a short tail
             work = L.m.astype(np.int64) * np.maximum(self.ncols.astype(np.int64), 1)
             order = np.argsort(-work, kind="stable").astype(np.int32)

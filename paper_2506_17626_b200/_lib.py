@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(HERE, "libfeatlsq_b200.so")
 FL_OK, FL_ERR_INVALID, FL_ERR_DEGENERATE, FL_ERR_DIVERGENCE, FL_ERR_SINGULAR, FL_ERR_CUDA = \
     0, -1, -2, -3, -4, -5
 FL_ROW_TILE, FL_COL_TILE, FL_ASM_TILE = 256, 32, 64
+FL_LSQR_SPLIT_MAX = 4
 
 p_d, p_i32, p_i64, p_u32 = (C.POINTER(C.c_double), C.POINTER(C.c_int32),
                             C.POINTER(C.c_int64), C.POINTER(C.c_uint32))

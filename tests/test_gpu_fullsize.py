@@ -1,0 +1,59 @@
+"""Full-size filtering parity against the REFERENCE run at BASELINE sizes.
+
+tests/golden/full_<cfg>.npz were produced by tests/golden/make_golden_full.py,
+which runs the reference's own `assemble` (assembly.py:124) and, per block,
+its `qr_column_pivot` (linalg.py:58) exactly as `filter_system`
+(filtering.py:92-115) does. The device pipeline (K1 assembly + route-R
+RRQR) must reproduce every per-block rank and kept sequence (pivot order)
+exactly and ||R_j||_F to 1e-10 relative.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FULL = ["cfg3", "cfg5", "cfg4"]
+
+
+@pytest.fixture(scope="module")
+def fl():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_17626_b200 as fl
+    return fl
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_kept_sequences_match_reference(fl, name, golden_dir):
+    path = os.path.join(golden_dir, f"full_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    import torch
+    from paper_2506_17626_b200 import workloads
+    g = np.load(path)
+    wl = workloads.build(name)
+    sysd = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    assert tuple(sysd.shape) == tuple(int(s) for s in g["shape"])
+    fs = fl.filter_system(sysd, wl.sigma)
+    assert np.array_equal(fs.ranks, g["ranks"])
+    K = fs.K
+    local = np.concatenate([k - j * K for j, k in enumerate(fs.kept_list)])
+    assert np.array_equal(local, g["kept"].astype(np.int64))
+    assert fs.kept_total == int(g["ranks"].sum())
+    # ||R_j||_F on the device over the leading rank x rank corner
+    J = len(fs.kept_list)
+    R = fs._R[:J * K * K].view(J, K, K)
+    r = torch.as_tensor(fs.ranks, device=R.device)
+    idx = torch.arange(K, device=R.device)
+    mask = (idx[None, :, None] < r[:, None, None]) & (idx[None, None, :] < r[:, None, None])
+    fro = torch.sqrt((torch.where(mask, R, torch.zeros((), dtype=R.dtype, device=R.device)) ** 2)
+                     .sum(dim=(1, 2))).cpu().numpy()
+    np.testing.assert_allclose(fro, g["r_fro"], rtol=1e-10)
+    del fs, sysd
+    torch.cuda.empty_cache()
