@@ -121,6 +121,13 @@ typedef struct fl_assembly_desc {
   const int32_t* con_grp;   /* constraint group */
   int32_t n_tiles;          /* row tiles of FL_ASM_TILE rows */
   const int32_t* tiles;     /* (n_tiles, 2): block, first row */
+  /* hard-constraint mask (assembly.py:107-114): the window jet along axis a
+     is multiplied by the mask's jet along a, given per point as (value,
+     d/dx_a, d2/dx_a^2); NULL = no mask */
+  const double* mask_int;   /* (n_interior, d, 3) interior lattice points, C order */
+  const double* mask_con;   /* (Ncp, d, 3) constraint points */
+  int64_t lattice_stride[3];/* C-order strides of the interior lattice (row id of a
+                               lattice point = sum_i index_i * stride_i) */
 } fl_assembly_desc;
 
 #define FL_ASM_TILE 64
@@ -175,6 +182,8 @@ typedef struct fl_lsqr_state {
   int32_t use_rule;
   int32_t stride;           /* monitor stride */
   int32_t nonfinite;        /* scratch flag set by any CTA seeing a non-finite x */
+  int32_t monitor;          /* 1 = best iterate by test error (fl_test_monitor), 0 = by residual */
+  int32_t improved;         /* test-error monitor: x of the last recorded iteration is the new best */
 } fl_lsqr_state;
 
 typedef struct fl_lsqr_vecs {
@@ -195,6 +204,38 @@ int fl_lsqr_init(const fl_blockop* op, const double* rhs, fl_lsqr_vecs* vecs,
  * budget (or capture it in a CUDA graph) without host synchronisation. */
 int fl_lsqr_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st,
                     int64_t first_it, int64_t count, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K6 — device test-lattice monitor (runner.py:265-276 `_error_matrix`,
+ * assembly.py:313-318 `l1_error`, solvers.py:59-69 `observe`). The error
+ * of the iterate y is e = mean_g |(T y)[g] + lift[g] - truth[g]| / spread
+ * with T_j = P_j[:, kept_j] R_j^{-1} (P = solution blocks at the test points).
+ * ---------------------------------------------------------------------- */
+typedef struct fl_test_monitor {
+  fl_blockop T;             /* rows = test points, ncols = r_j, col_off = y offsets */
+  const double* lift;       /* (n_test,) lift values at the test points */
+  const double* truth;      /* (n_test,) true values */
+  double spread;            /* std of the true values */
+  double* err_trace;        /* (max_iters + 1,) e per recorded iteration */
+  double* result;           /* (1,) output of fl_monitor_error */
+} fl_test_monitor;
+
+/* T_j = P_j[:, perm_j[0:r_j]] R_j^{-1} row by row (forward substitution with
+ * R_j^T); r_j = T->ncols[j]. `tiles` = (n_tiles, 2) (block, first row) in
+ * steps of FL_TBUILD_ROWS rows. P and T share one layout. */
+int fl_error_blocks(const fl_blockop* P, const double* R, const int32_t* perm, int32_t K,
+                    const fl_blockop* T, int32_t n_tiles, const int32_t* tiles, void* stream);
+#define FL_TBUILD_ROWS 16
+/* e(y) -> mon->result[0] */
+int fl_monitor_error(const fl_test_monitor* mon, const double* y, void* stream);
+/* fl_lsqr_iterate plus, after each recorded iteration (stride), e(x_it) ->
+ * err_trace[it] and the best iterate by e (st->monitor must be 1); call
+ * fl_lsqr_monitor_flush after the last iteration. */
+int fl_lsqr_iterate_monitored(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st,
+                              int64_t first_it, int64_t count, const fl_test_monitor* mon,
+                              void* stream);
+/* copies x into xbest if the last recorded iterate improved the best */
+int fl_lsqr_monitor_flush(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, void* stream);
 
 /* ------------------------------------------------------------------------
  * Recovery (filtering.py:169-183): coeffs[kept global column] = R_j^{-1} y_j,

@@ -136,8 +136,10 @@ def operator_rows(op, problem, dec, basis, j, pts):
     jets = []
     for a in range(dec.dim):
         w = window_jet(dec, j, pts, a)
-        if problem.mask_jets is not None:
-            raise NotImplementedError("mask/lift problems are outside the oracle's scope")
+        if problem.mask_jets is not None:  # window * mask (assembly.py:111-112)
+            mk = problem.mask_jets(pts, a)
+            w = _mul(w, (np.broadcast_to(mk.value, w[0].shape), np.broadcast_to(mk.first, w[0].shape),
+                         np.broadcast_to(mk.second, w[0].shape)))
         wj = (w[0][:, None], w[1][:, None], w[2][:, None])
         jets.append(_mul(wj, feature_jet(basis, j, pts, a)))
     out = op.value_coef * jets[0][0]
@@ -147,15 +149,45 @@ def operator_rows(op, problem, dec, basis, j, pts):
 
 
 # ---------------------------------------------------------------------------
-# assembly (assembly.py:124-238), mask-free problems
+# assembly (assembly.py:124-238), including hard-constraint mask/lift problems
+
+def default_counts(problem, dec, basis):
+    """assembly.py:32-40 + :141-146 (one extra point per subdomain when masked)."""
+    k, d = basis.feature_count, dec.dim
+    root = int(np.ceil(k ** (1.0 / d)))
+    while root > 1 and (root - 1) ** d >= k:
+        root -= 1
+    while root ** d < k:
+        root += 1
+    extra = 0 if problem.mask_jets is None else 1
+    return dec.count_per_dim * (root + extra)
+
 
 def lattice_axes(problem, dec, basis, interior_per_dim):
     d = dec.dim
+    if interior_per_dim is None:
+        interior_per_dim = default_counts(problem, dec, basis)
     counts = ((int(interior_per_dim),) * d if not isinstance(interior_per_dim, (tuple, list))
               else tuple(int(c) for c in interior_per_dim))
-    axes = tuple(np.linspace(dec.domain.bounds[i, 0], dec.domain.bounds[i, 1], counts[i])
-                 for i in range(d))
+    if problem.mask_jets is None:
+        axes = tuple(np.linspace(dec.domain.bounds[i, 0], dec.domain.bounds[i, 1], counts[i])
+                     for i in range(d))
+    else:  # cell centres (assembly.py:159-166)
+        steps = dec.domain.widths / np.asarray(counts)
+        axes = tuple(dec.domain.bounds[i, 0] + steps[i] * (np.arange(counts[i]) + 0.5)
+                     for i in range(d))
     return counts, axes
+
+
+def lift_operator_values(problem, op, pts):
+    """assembly.py:117-121."""
+    if problem.lift_jets is None:
+        return np.zeros(np.atleast_2d(pts).shape[0])
+    jets = [problem.lift_jets(pts, a) for a in range(problem.domain.dim)]
+    out = op.value_coef * jets[0].value
+    for a, jet in enumerate(jets):
+        out = out + op.first_coefs[a] * jet.first + op.second_coefs[a] * jet.second
+    return out
 
 
 def assemble(problem, dec, basis, interior_per_dim, only=None):
@@ -168,12 +200,13 @@ def assemble(problem, dec, basis, interior_per_dim, only=None):
     interior = np.stack([m.ravel() for m in mesh], axis=1)
     n_int = interior.shape[0]
     iw = 1.0 / np.sqrt(n_int)
-    rhs = [problem.forcing(interior) * iw]
+    rhs = [(problem.forcing(interior) - lift_operator_values(problem, problem.operator, interior)) * iw]
     con_off, off = [], n_int
     for con in problem.constraints:
         n_con = con.points.shape[0]
         w = np.sqrt(con.weight / n_con)
-        rhs.append(np.asarray(con.targets, float) * w)
+        rhs.append((np.asarray(con.targets, float)
+                    - lift_operator_values(problem, con.operator, con.points)) * w)
         con_off.append((off, w))
         off += n_con
     k = basis.feature_count
@@ -446,15 +479,19 @@ def test_lattice(problem, dec):
     return pts, truth, float(np.std(truth))
 
 
-def solution_csr(dec, basis, pts):
+def solution_csr(dec, basis, pts, problem=None):
+    """assembly.py:244-272 (P only; the lift is `lift_values`)."""
     rows, cols, vals = [], [], []
     k = basis.feature_count
+    mask = problem.mask_value(pts) if problem is not None and problem.mask_value else None
     for j in range(dec.subdomain_count):
         inside = np.nonzero(support(dec, j, pts))[0]
         if inside.size == 0:
             continue
         p = pts[inside]
         w = window_jet(dec, j, p, 0)[0]
+        if mask is not None:
+            w = w * mask[inside]
         phi = feature_jet(basis, j, p, 0)[0]
         rows.append(np.repeat(inside, k))
         cols.append(np.tile(np.arange(j * k, (j + 1) * k), inside.size))
@@ -464,24 +501,20 @@ def solution_csr(dec, basis, pts):
         shape=(pts.shape[0], basis.column_count)).tocsr()
 
 
+def lift_values(problem, pts):
+    return problem.lift_value(pts) if problem.lift_value else np.zeros(np.atleast_2d(pts).shape[0])
+
+
 def run_rrqr_lsqr(problem, dec, basis, sigma, max_iters, interior_per_dim=None):
     """One seed of `runner._solve_one` for solver rrqr-lsqr, eval_stride 1.
     Returns dict(error, best_iteration, iterations, residual, drop_fraction,
     kept, coeffs)."""
-    if interior_per_dim is None:
-        # assembly.py:32-40 + :141-146, mask-free
-        k, d = basis.feature_count, dec.dim
-        root = int(np.ceil(k ** (1.0 / d)))
-        while root > 1 and (root - 1) ** d >= k:
-            root -= 1
-        while root ** d < k:
-            root += 1
-        interior_per_dim = dec.count_per_dim * root
     sysd = assemble(problem, dec, basis, interior_per_dim)
     fb, off = filter_system(sysd, sigma)
     q = q_operator(fb, off, sysd["row_count"])
     pts, truth, spread = test_lattice(problem, dec)
-    phi = solution_csr(dec, basis, pts)
+    phi = solution_csr(dec, basis, pts, problem)
+    lift = lift_values(problem, pts)
     kept = np.concatenate([b["kept"] for b in fb])
     sinv = scipy.sparse.block_diag(
         [scipy.linalg.solve_triangular(b["r"], np.eye(b["kept"].size)) for b in fb],
@@ -490,14 +523,14 @@ def run_rrqr_lsqr(problem, dec, basis, sigma, max_iters, interior_per_dim=None):
     best = dict(err=np.inf, it=-1, x=None)
 
     def observe(it, x, _phibar):
-        err = float(np.mean(np.abs(t_mat @ x - truth)) / spread)
+        err = float(np.mean(np.abs(t_mat @ x + lift - truth)) / spread)
         if err < best["err"]:
             best.update(err=err, it=it, x=x.copy())
     x, its, phibar, _, _ = lsqr(lambda v: q @ v, lambda r: q.T @ r, int(off[-1]),
                                 sysd["rhs"], max_iters, observe)
     y = best["x"] if best["x"] is not None else x
     coeffs = recover_solution(fb, off, y, sysd["column_count"])
-    err = float(np.mean(np.abs(phi @ coeffs - truth)) / spread)
+    err = float(np.mean(np.abs(phi @ coeffs + lift - truth)) / spread)
     return dict(error=err, best_iteration=best["it"], iterations=its, residual=phibar,
                 drop_fraction=1.0 - off[-1] / sysd["column_count"], kept=int(off[-1]),
                 coeffs=coeffs)

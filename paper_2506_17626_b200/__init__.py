@@ -5,7 +5,9 @@ reference stage API (featlsq assembly.py:124, filtering.py:92/165/169,
 solvers.py:87). Kernels: csrc/*.cu, C-ABI: include/featlsq_b200.h.
 """
 
-from .assembly import GlobalSystem, SubdomainBlock, apply, apply_transpose, assemble
+from .assembly import (GlobalSystem, SolutionBlocks, SubdomainBlock, TestSet, apply,
+                       apply_transpose, assemble, evaluate_solution, l1_error, make_test_set,
+                       solution_matrix)
 from .basis import ACTIVATIONS, FeatureBasis, init_basis
 from .domains import Decomposition, Domain, decompose
 from .errors import (CapExceededError, CoverageError, DegenerateSubdomainError, DeviceError,
@@ -13,7 +15,10 @@ from .errors import (CapExceededError, CoverageError, DegenerateSubdomainError, 
 from .filtering import (FilteredBlock, FilteredSystem, PreconditionedOperator, filter_system,
                         precondition, recover_solution)
 from .linalg import PivotedQR, RandomSource, back_substitute, lattice_counts, qr_column_pivot
-from .problems import ConstraintRows, LinearOperator2, ProblemSpec, oscillator_problem
+from .jets import Jet2, radial_jet
+from .monitor import DeviceL1Error, test_error_fn
+from .problems import (ConstraintRows, LinearOperator2, ProblemSpec, laplace_problem,
+                       oscillator_problem, wave_problem)
 from .solvers import ConvergenceMonitor, Operator, SolveResult, as_operator, lsqr
 
 __version__ = "0.1.0"
@@ -27,4 +32,7 @@ __all__ = [
     "apply_transpose", "as_operator", "assemble", "back_substitute", "decompose",
     "filter_system", "init_basis", "lattice_counts", "lsqr", "oscillator_problem",
     "precondition", "qr_column_pivot", "recover_solution",
+    "DeviceL1Error", "Jet2", "SolutionBlocks", "TestSet", "evaluate_solution", "l1_error",
+    "laplace_problem", "make_test_set", "radial_jet", "solution_matrix", "test_error_fn",
+    "wave_problem",
 ]

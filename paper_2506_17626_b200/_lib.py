@@ -20,6 +20,7 @@ FL_OK, FL_ERR_INVALID, FL_ERR_DEGENERATE, FL_ERR_DIVERGENCE, FL_ERR_SINGULAR, FL
     0, -1, -2, -3, -4, -5
 FL_ROW_TILE, FL_COL_TILE, FL_ASM_TILE = 256, 32, 64
 FL_LSQR_SPLIT_MAX = 4
+FL_TBUILD_ROWS = 16
 
 p_d, p_i32, p_i64, p_u32 = (C.POINTER(C.c_double), C.POINTER(C.c_int32),
                             C.POINTER(C.c_int64), C.POINTER(C.c_uint32))
@@ -49,6 +50,7 @@ class AssemblyDesc(C.Structure):
         ("op_coef", C.c_void_p), ("con_pts", C.c_void_p), ("box", C.c_void_p),
         ("con_ptr", C.c_void_p), ("con_idx", C.c_void_p), ("con_grp", C.c_void_p),
         ("n_tiles", C.c_int32), ("tiles", C.c_void_p),
+        ("mask_int", C.c_void_p), ("mask_con", C.c_void_p), ("lattice_stride", C.c_int64 * 3),
     ]
 
 
@@ -60,11 +62,17 @@ class LsqrState(C.Structure):
         ("it", C.c_int64), ("best_it", C.c_int64), ("diverged_at", C.c_int64),
         ("done", C.c_int32), ("breakdown", C.c_int32), ("istop", C.c_int32),
         ("use_rule", C.c_int32), ("stride", C.c_int32), ("nonfinite", C.c_int32),
+        ("monitor", C.c_int32), ("improved", C.c_int32),
     ]
 
 
 class LsqrVecs(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("u", "v", "vp", "w", "x", "xbest", "trace")]
+
+
+class TestMonitor(C.Structure):
+    _fields_ = [("T", BlockOp), ("lift", C.c_void_p), ("truth", C.c_void_p), ("spread", C.c_double),
+                ("err_trace", C.c_void_p), ("result", C.c_void_p)]
 
 
 _lib = None
@@ -95,6 +103,12 @@ def lib():
                             C.c_double, vp, vp, vp, vp, vp, vp],
         "fl_dev_wy_apply": [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
                             C.c_int32, vp, vp, C.c_int32, vp],
+        "fl_error_blocks": [C.POINTER(BlockOp), vp, vp, C.c_int32, C.POINTER(BlockOp), C.c_int32,
+                            vp, vp],
+        "fl_monitor_error": [C.POINTER(TestMonitor), vp, vp],
+        "fl_lsqr_iterate_monitored": [C.POINTER(BlockOp), C.POINTER(LsqrVecs), vp, C.c_int64,
+                                      C.c_int64, C.POINTER(TestMonitor), vp],
+        "fl_lsqr_monitor_flush": [C.POINTER(BlockOp), C.POINTER(LsqrVecs), vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -112,7 +126,9 @@ def lib():
 
 EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", "fl_lsqr_init",
             "fl_lsqr_iterate", "fl_backsub_scatter", "fl_probe_fp64", "fl_dev_wy_apply",
-            "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error")
+            "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error",
+            "fl_error_blocks", "fl_monitor_error", "fl_lsqr_iterate_monitored",
+            "fl_lsqr_monitor_flush")
 
 
 def check(code: int, what: str) -> None:

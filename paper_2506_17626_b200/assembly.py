@@ -25,6 +25,7 @@ from . import _lib
 from .basis import ACTIVATIONS
 from .domains import support_runs
 from .errors import CapExceededError, CoverageError, InvalidInputError
+from .jets import triples
 
 DENSE_SIZE_CAP = 20_000
 
@@ -189,6 +190,60 @@ def _layout_inputs(problem, dec, basis, axes, counts):
             rows_per_block)
 
 
+def _lift_values(problem, operator, points) -> np.ndarray:
+    """Operator applied to the lift jets (`assembly.py:117-121`), zeros without a lift."""
+    pts = np.atleast_2d(points)
+    if problem.lift_jets is None:
+        return np.zeros(pts.shape[0])
+    jets = [problem.lift_jets(pts, a) for a in range(problem.domain.dim)]
+    return _apply_operator(operator, jets)
+
+
+def _apply_operator(op, jets) -> np.ndarray:
+    """`problems.py:39-47` (same term order), for duck-typed operators."""
+    out = op.value_coef * jets[0].value
+    for a, jet in enumerate(jets):
+        out = out + op.first_coefs[a] * jet.first + op.second_coefs[a] * jet.second
+    return out
+
+
+def _make_desc(dec, basis, layout, axes, coef_rows, con_pts, box, con_ptr, con_idx, con_grp,
+               ngroups, mask_int, mask_con, counts):
+    """Upload the K1 inputs and build the `fl_assembly_desc`."""
+    d, J, K = dec.dim, dec.subdomain_count, basis.feature_count
+    tiles = D.tile_table(layout.ld, _lib.FL_ASM_TILE)
+    keep = dict(
+        centers=D.to_dev(np.asarray(dec.centers, float)),
+        half=D.to_dev(np.asarray(dec.half_widths, float)),
+        weights=D.to_dev(np.asarray(basis.weights[0], float).reshape(J, K, d)),
+        biases=D.to_dev(np.asarray(basis.biases[0], float).reshape(J, K)
+                        if basis.biases[0] is not None else np.zeros((J, K))),
+        axes=D.to_dev(np.concatenate(axes) if len(axes) else np.zeros(1)),
+        axis_off=D.to_dev(np.cumsum([0] + [a.size for a in axes[:-1]]).astype(np.int64)
+                          if len(axes) else np.zeros(d, np.int64)),
+        op_coef=D.to_dev(np.array(coef_rows, dtype=float)),
+        con_pts=D.to_dev(con_pts if con_pts.shape[0] else np.zeros((1, d))),
+        box=D.to_dev(box), con_ptr=D.to_dev(con_ptr), con_idx=D.to_dev(con_idx.astype(np.int32)),
+        con_grp=D.to_dev(con_grp.astype(np.int32)), tiles=D.to_dev(tiles))
+    if mask_int is not None:
+        keep["mask_int"] = D.to_dev(mask_int)
+    if mask_con is not None:
+        keep["mask_con"] = D.to_dev(mask_con)
+    stride = (C.c_int64 * 3)(*([int(np.prod(counts[i + 1:])) for i in range(d)] + [0] * (3 - d)))
+    desc = _lib.AssemblyDesc(
+        dim=d, nsub=J, count_per_dim=dec.count_per_dim, nfeat=K,
+        activation=ACTIVATIONS[basis.activation], ngroups=ngroups,
+        reach=int(np.ceil(dec.overlap_ratio)) + 1,
+        centers=D.ptr(keep["centers"]), half=D.ptr(keep["half"]), weights=D.ptr(keep["weights"]),
+        biases=D.ptr(keep["biases"]), axes=D.ptr(keep["axes"]), axis_off=D.ptr(keep["axis_off"]),
+        op_coef=D.ptr(keep["op_coef"]), con_pts=D.ptr(keep["con_pts"]), box=D.ptr(keep["box"]),
+        con_ptr=D.ptr(keep["con_ptr"]), con_idx=D.ptr(keep["con_idx"]),
+        con_grp=D.ptr(keep["con_grp"]), n_tiles=len(tiles), tiles=D.ptr(keep["tiles"]),
+        mask_int=D.ptr(keep.get("mask_int")), mask_con=D.ptr(keep.get("mask_con")),
+        lattice_stride=stride)
+    return keep, desc
+
+
 class AssemblyPlan:
     """Everything `assemble` derives on the host, uploaded once: the layout,
     the right-hand side and the K1 descriptor. `launch(vals)` re-runs only
@@ -197,9 +252,16 @@ class AssemblyPlan:
     def __init__(self, problem, dec, basis, interior_per_dim=None):
         _validate(problem, dec, basis)
         d = dec.dim
-        counts = _lattice_counts(dec, basis, interior_per_dim)
-        axes = tuple(np.linspace(dec.domain.bounds[i, 0], dec.domain.bounds[i, 1], counts[i])
-                     for i in range(d))
+        masked = problem.mask_jets is not None
+        counts = _lattice_counts(dec, basis, interior_per_dim, extra=1 if masked else 0)
+        if not masked:
+            axes = tuple(np.linspace(dec.domain.bounds[i, 0], dec.domain.bounds[i, 1], counts[i])
+                         for i in range(d))
+        else:
+            # cell centres for hard-constrained problems (assembly.py:159-166)
+            steps = dec.domain.widths / np.asarray(counts)
+            axes = tuple(dec.domain.bounds[i, 0] + steps[i] * (np.arange(counts[i]) + 0.5)
+                         for i in range(d))
         n_interior = int(np.prod(counts))
         _coverage(problem, dec, axes, n_interior)
 
@@ -207,14 +269,16 @@ class AssemblyPlan:
         mesh = np.meshgrid(*axes, indexing="ij")
         interior = np.stack([m.ravel() for m in mesh], axis=1)
         iw = 1.0 / np.sqrt(n_interior)
-        rhs_parts = [(np.asarray(problem.forcing(interior), dtype=float) - np.zeros(n_interior)) * iw]
+        rhs_parts = [(np.asarray(problem.forcing(interior), dtype=float)
+                      - _lift_values(problem, problem.operator, interior)) * iw]
         coef_rows = [[float(problem.operator.value_coef), iw, *problem.operator.first_coefs,
                       *problem.operator.second_coefs]]
         con_pts = []
         for con in problem.constraints:
             pts = np.atleast_2d(np.asarray(con.points, dtype=float))
             w = np.sqrt(con.weight / pts.shape[0])
-            rhs_parts.append((np.asarray(con.targets, dtype=float) - np.zeros(pts.shape[0])) * w)
+            rhs_parts.append((np.asarray(con.targets, dtype=float)
+                              - _lift_values(problem, con.operator, pts)) * w)
             op = con.operator
             coef_rows.append([float(op.value_coef), w, *op.first_coefs, *op.second_coefs])
             con_pts.append(pts)
@@ -227,33 +291,18 @@ class AssemblyPlan:
         goff = np.cumsum([0] + [p.shape[0] for p in con_pts])
         con_idx = con_idx + goff[con_grp].astype(np.int32) if con_idx.size else con_idx
         K = basis.feature_count
-        J = dec.subdomain_count
         self.layout = D.BlockLayout(row_count, K, rows_per_block)
         self.rows_per_block = rows_per_block
         self.problem, self.dec, self.basis = problem, dec, basis
         self.axes, self.n_interior, self.row_count = axes, n_interior, row_count
-        tiles = D.tile_table(self.layout.ld, _lib.FL_ASM_TILE)
-        self.keep = keep = dict(
-            centers=D.to_dev(np.asarray(dec.centers, float)),
-            half=D.to_dev(np.asarray(dec.half_widths, float)),
-            weights=D.to_dev(np.asarray(basis.weights[0], float).reshape(J, K, d)),
-            biases=D.to_dev(np.asarray(basis.biases[0], float).reshape(J, K)
-                            if basis.biases[0] is not None else np.zeros((J, K))),
-            axes=D.to_dev(np.concatenate(axes)),
-            axis_off=D.to_dev(np.cumsum([0] + [a.size for a in axes[:-1]]).astype(np.int64)),
-            op_coef=D.to_dev(np.array(coef_rows, dtype=float)),
-            con_pts=D.to_dev(np.concatenate(con_pts) if con_pts else np.zeros((1, d))),
-            box=D.to_dev(box), con_ptr=D.to_dev(con_ptr), con_idx=D.to_dev(con_idx.astype(np.int32)),
-            con_grp=D.to_dev(con_grp.astype(np.int32)), tiles=D.to_dev(tiles))
-        self.desc = _lib.AssemblyDesc(
-            dim=d, nsub=J, count_per_dim=dec.count_per_dim, nfeat=K,
-            activation=ACTIVATIONS[basis.activation], ngroups=len(problem.constraints),
-            reach=int(np.ceil(dec.overlap_ratio)) + 1,
-            centers=D.ptr(keep["centers"]), half=D.ptr(keep["half"]), weights=D.ptr(keep["weights"]),
-            biases=D.ptr(keep["biases"]), axes=D.ptr(keep["axes"]), axis_off=D.ptr(keep["axis_off"]),
-            op_coef=D.ptr(keep["op_coef"]), con_pts=D.ptr(keep["con_pts"]), box=D.ptr(keep["box"]),
-            con_ptr=D.ptr(keep["con_ptr"]), con_idx=D.ptr(keep["con_idx"]),
-            con_grp=D.ptr(keep["con_grp"]), n_tiles=len(tiles), tiles=D.ptr(keep["tiles"]))
+        all_con = np.concatenate(con_pts) if con_pts else np.zeros((0, d))
+        mask_int = mask_con = None
+        if masked:  # per-point mask jets along every axis (assembly.py:111-112)
+            mask_int = triples(problem.mask_jets, interior, d)
+            mask_con = triples(problem.mask_jets, all_con, d) if all_con.shape[0] else None
+        self.keep, self.desc = _make_desc(
+            dec, basis, self.layout, axes, coef_rows, all_con, box, con_ptr, con_idx, con_grp,
+            len(problem.constraints), mask_int, mask_con, counts)
 
     def new_store(self) -> D.DeviceBlocks:
         t = D.torch()
@@ -281,9 +330,6 @@ def _validate(problem, dec, basis):
         raise InvalidInputError("basis was initialized on a different decomposition")
     if not np.array_equal(problem.domain.bounds, dec.domain.bounds):
         raise InvalidInputError("problem and decomposition domains differ")
-    if problem.mask_jets is not None or problem.lift_jets is not None:
-        raise NotImplementedError(
-            "hard-constraint (mask/lift) problems are not on the accelerated path yet")
     if basis.depth != 1:
         raise NotImplementedError("only depth-1 feature networks are on the accelerated path")
     if basis.activation not in ACTIVATIONS:
@@ -292,11 +338,12 @@ def _validate(problem, dec, basis):
         raise NotImplementedError("dimension > 3 is not on the accelerated path")
 
 
-def _lattice_counts(dec, basis, interior_per_dim):
+def _lattice_counts(dec, basis, interior_per_dim, extra=0):
     d = dec.dim
     if interior_per_dim is None:
+        # masked problems get one extra point per subdomain and dimension (assembly.py:141-145)
         from .linalg import lattice_counts
-        return (lattice_counts(dec.count_per_dim, basis.feature_count, d, 0),) * d
+        return (lattice_counts(dec.count_per_dim, basis.feature_count, d, extra),) * d
     counts = (tuple(int(c) for c in interior_per_dim)
               if isinstance(interior_per_dim, (tuple, list))
               else (int(interior_per_dim),) * d)
@@ -329,3 +376,138 @@ def assemble(problem, dec, basis, interior_per_dim=None) -> GlobalSystem:
     store = plan.new_store()
     plan.launch(store)
     return plan.system(store)
+
+
+# ---------------------------------------------------------------------------
+# prediction and testing (assembly.py:244-318): K1 evaluates the solution
+# blocks at arbitrary points (value operator, unit weight, mask values)
+
+class SolutionBlocks:
+    """Device blocks P_j = mask * window_j * features_j at the points inside
+    subdomain j (rows = point indices), plus the lift values: predictions are
+    P a + lift (`assembly.py:244-272`)."""
+
+    def __init__(self, problem, dec, basis, points):
+        _validate(problem, dec, basis)
+        pts = np.atleast_2d(np.asarray(points, dtype=float))
+        n, d = pts.shape[0], dec.dim
+        if d != pts.shape[1]:
+            raise InvalidInputError(f"points must have {d} columns, got {pts.shape[1]}")
+        J, K, S = dec.subdomain_count, basis.feature_count, dec.count_per_dim
+        mem = _member(dec, pts)
+        multi = np.array(np.unravel_index(np.arange(J), (S,) * d)).T
+        rows = []
+        for j in range(J):
+            inside = mem[0, multi[j, 0]].copy()
+            for i in range(1, d):
+                inside &= mem[i, multi[j, i]]
+            rows.append(np.nonzero(inside)[0])
+        sizes = np.array([r.size for r in rows], dtype=np.int64)
+        con_ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        con_idx = np.concatenate(rows).astype(np.int32) if J else np.zeros(0, np.int32)
+        coef_rows = [[0.0] * (2 + 2 * d), [1.0, 1.0] + [0.0] * (2 * d)]
+        mask_con = None
+        if problem.mask_value is not None and n:
+            mv = np.asarray(problem.mask_value(pts), dtype=float)
+            mask_con = np.zeros((n, d, 3))
+            mask_con[:, :, 0] = mv[:, None]
+        self.layout = D.BlockLayout(n, K, rows)
+        self.rows = rows
+        self.points = pts
+        self.column_count = basis.column_count
+        self.lift = (np.asarray(problem.lift_value(pts), dtype=float) if problem.lift_value
+                     else np.zeros(n))
+        keep, desc = _make_desc(dec, basis, self.layout, (), coef_rows, pts,
+                                np.zeros((J, d, 2), np.int32), con_ptr, con_idx,
+                                np.zeros(con_idx.size, np.int32), 1, None, mask_con, (0,) * d)
+        t = D.torch()
+        vals = t.empty(max(self.layout.total, 1), dtype=t.float64, device=D.require_cuda())
+        self.store = D.DeviceBlocks(self.layout, vals, np.full(J, K, np.int32),
+                                    np.arange(J, dtype=np.int64) * K)
+        if self.layout.J:
+            _lib.check(_lib.lib().fl_assemble(C.byref(desc), C.byref(self.store.struct()),
+                                              D.stream_ptr()), "fl_assemble")
+        self._keep = keep
+        self._csr = None
+
+    def csr(self) -> scipy.sparse.csr_matrix:
+        if self._csr is None:
+            K = self.layout.K
+            mats = self.store.all_blocks_host()
+            r, c, v = [], [], []
+            for j, (inside, mat) in enumerate(zip(self.rows, mats)):
+                if inside.size == 0:
+                    continue
+                r.append(np.repeat(inside, K))
+                c.append(np.tile(np.arange(j * K, (j + 1) * K), inside.size))
+                v.append(mat.ravel())
+            n = self.points.shape[0]
+            if r:
+                self._csr = scipy.sparse.coo_matrix(
+                    (np.concatenate(v), (np.concatenate(r), np.concatenate(c))),
+                    shape=(n, self.column_count)).tocsr()
+            else:
+                self._csr = scipy.sparse.csr_matrix((n, self.column_count))
+        return self._csr
+
+    def predict_device(self, coeffs_dev):
+        """P a + lift on the device (n,)."""
+        out = self.store.apply(coeffs_dev)[:self.points.shape[0]]
+        return out + D.torch().from_numpy(self.lift).to(out.device)
+
+
+def solution_blocks(problem, dec, basis, points) -> SolutionBlocks:
+    return SolutionBlocks(problem, dec, basis, points)
+
+
+def solution_matrix(problem, dec, basis, points):
+    """(CSR P, lift) with predictions P a + lift (`assembly.py:244-272`);
+    P's entries are evaluated on the device."""
+    sb = SolutionBlocks(problem, dec, basis, points)
+    return sb.csr(), sb.lift
+
+
+def evaluate_solution(problem, dec, basis, coeffs, points) -> np.ndarray:
+    """mask * sum_j window_j sum_k a_jk feature_jk + lift (`assembly.py:275-283`)."""
+    coeffs = np.asarray(coeffs, dtype=float)
+    if coeffs.shape != (basis.column_count,):
+        raise InvalidInputError(f"coefficients must have shape ({basis.column_count},)")
+    sb = SolutionBlocks(problem, dec, basis, points)
+    if sb.points.shape[0] == 0:
+        return np.zeros(0)
+    return D.to_host(sb.predict_device(D.to_dev(coeffs)))
+
+
+@dataclass(frozen=True)
+class TestSet:
+    """Evaluation lattice with true values and their spread (`assembly.py:286-292`)."""
+
+    points: np.ndarray
+    true_values: np.ndarray
+    spread: float
+
+
+def make_test_set(problem, dec) -> TestSet:
+    """problem.test_points_per_count * count points per dimension
+    (`assembly.py:295-310`)."""
+    if problem.exact is None:
+        raise InvalidInputError(
+            f"problem {problem.name!r} has no exact or reference solution attached")
+    per_dim = problem.test_points_per_count * dec.count_per_dim
+    axes = [np.linspace(problem.domain.bounds[i, 0], problem.domain.bounds[i, 1], per_dim)
+            for i in range(problem.domain.dim)]
+    mesh = np.meshgrid(*axes, indexing="ij")
+    points = np.stack([m.ravel() for m in mesh], axis=1)
+    true_values = problem.exact(points)
+    spread = float(np.std(true_values))
+    if spread == 0.0:
+        raise InvalidInputError("true solution has zero spread on the test lattice")
+    return TestSet(points, true_values, spread)
+
+
+def l1_error(predicted, test_set: TestSet) -> float:
+    """Mean absolute error over the spread of the truth (`assembly.py:313-318`)."""
+    predicted = np.asarray(predicted, dtype=float)
+    if predicted.shape != test_set.true_values.shape:
+        raise InvalidInputError("prediction and truth shapes differ")
+    return float(np.mean(np.abs(predicted - test_set.true_values)) / test_set.spread)

@@ -118,20 +118,25 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
       const int32_t* box = d.box + (int64_t)j * D * 2;
       int boxcount = 1;
       for (int i = 0; i < D; ++i) boxcount *= box[2 * i + 1];
+      const double* mk = nullptr;  // mask jets of this point, (D, 3)
       if (r < boxcount) {
         int rem = r;
+        int64_t gid = 0;
         for (int i = D - 1; i >= 0; --i) {
           int cnt = box[2 * i + 1];
           int digit = rem % cnt;
           rem /= cnt;
           x[i] = d.axes[d.axis_off[i] + box[2 * i] + digit];
+          gid += (int64_t)(box[2 * i] + digit) * d.lattice_stride[i];
         }
         ri.coef = 0;
+        if (d.mask_int) mk = d.mask_int + gid * D * 3;
       } else {
         int64_t e = d.con_ptr[j] + (r - boxcount);
         int pi = d.con_idx[e];
         for (int i = 0; i < D; ++i) x[i] = d.con_pts[(int64_t)pi * D + i];
         ri.coef = 1 + d.con_grp[e];
+        if (d.mask_con) mk = d.mask_con + (int64_t)pi * D * 3;
       }
       // per-dim normalised factors: value-only and full jets
       double fval[MAXD];
@@ -163,6 +168,7 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
           Jet fi = (i == a) ? ffull[i] : Jet{fval[i], 0.0, 0.0};
           w = (i == 0) ? fi : jmul(w, fi);
         }
+        if (mk) w = jmul(w, Jet{mk[3 * a], mk[3 * a + 1], mk[3 * a + 2]});  // window * mask (assembly.py:111-112)
         if (a == 0) ri.wv = w.v;
         ri.wd1[a] = w.f;
         ri.wd2[a] = w.s;

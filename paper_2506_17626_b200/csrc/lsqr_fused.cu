@@ -129,14 +129,18 @@ __global__ void __launch_bounds__(NT, MB)
   } else {
     const double step = st->phi / st->rho;
     const bool record = (st->stride <= 1 || it % st->stride == 0);
-    improve = record && (phibar < st->best);
+    // best iterate: by residual here, or (test-error monitor, monitor.cu) the
+    // previous recorded x when its error was the new best
+    const bool mon = st->monitor;
+    improve = mon ? (*(volatile const int32_t*)&st->improved != 0) : (record && (phibar < st->best));
     int bad = 0;
     for (int c = threadIdx.x; c < ncr; c += NT) {
       const double wc = vec.w[cob + c];
-      const double xn = vec.x[cob + c] + step * wc;
+      const double xo = vec.x[cob + c];
+      const double xn = xo + step * wc;
       vec.x[cob + c] = xn;
       bad |= !isfinite(xn);
-      if (improve) vec.xbest[cob + c] = xn;
+      if (improve) vec.xbest[cob + c] = mon ? xo : xn;
       wss += wc * wc;
     }
     if (bad) atomicOr(&s_bad, 1);
@@ -279,12 +283,13 @@ __global__ void __launch_bounds__(NT, MB)
     return;
   }
   st->it = it;
+  if (st->monitor) st->improved = 0;  // every CTA has read it
   if (*(volatile int32_t*)&st->nonfinite) {  // DivergenceError at iteration it
     st->diverged_at = it;
     st->done = 1;
     return;
   }
-  if (improve) {
+  if (improve && !st->monitor) {
     st->best = phibar;
     st->best_it = it;
   }
@@ -497,8 +502,9 @@ int lsqr_fused_init(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st,
   if (!sh) return FL_ERR_INVALID;
   return fused(op, vecs, st, 0, 0, split_of(op, *sh), s);
 }
+int monitor_step(const fl_test_monitor* mon, const double* x, fl_lsqr_state* st, int64_t it, cudaStream_t s);
 int lsqr_fused_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t first_it,
-                       int64_t count, cudaStream_t s) {
+                       int64_t count, const fl_test_monitor* mon, cudaStream_t s) {
   const Shape* sh = shape_of(op);
   if (!sh) return FL_ERR_INVALID;
   const int S = split_of(op, *sh);
@@ -509,6 +515,7 @@ int lsqr_fused_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* 
     FL_CHECK_LAUNCH();
     int e = fused(op, vecs, st, it, 1, S, s);
     if (e) return e;
+    if (mon && (e = monitor_step(mon, vecs->x, st, it, s))) return e;
   }
   return FL_OK;
 }

@@ -29,8 +29,9 @@
 namespace fl {
 bool fused_ok(const fl_blockop* op);
 int lsqr_fused_init(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, cudaStream_t s);
+int monitor_step(const fl_test_monitor* mon, const double* x, fl_lsqr_state* st, int64_t it, cudaStream_t s);
 int lsqr_fused_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t first_it,
-                       int64_t count, cudaStream_t s);
+                       int64_t count, const fl_test_monitor* mon, cudaStream_t s);
 }  // namespace fl
 
 namespace {
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(NT) lsqr_qtu_kernel(fl_blockop op, fl_lsqr_vec
   const double step = st->phi / st->rho;
   const double phibar = st->phibar;
   const bool record = (st->stride <= 1 || it % st->stride == 0);
-  const bool improve = record && (phibar < st->best);
+  const bool mon = st->monitor;  // test-error monitor: copy the previous x when it was the best
+  const bool improve = mon ? (*(volatile const int32_t*)&st->improved != 0) : (record && (phibar < st->best));
   if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
   // x = x + (phi/rho) w; finiteness; monitor best iterate (solvers.py:128-132, 59-69)
@@ -198,10 +200,11 @@ __global__ void __launch_bounds__(NT) lsqr_qtu_kernel(fl_blockop op, fl_lsqr_vec
     int bad = 0;
     for (int c = c0 + threadIdx.x; c < c0 + CT && c < nc; c += NT) {
       const double wc = vec.w[co + c];
-      const double xn = vec.x[co + c] + step * wc;
+      const double xo = vec.x[co + c];
+      const double xn = xo + step * wc;
       vec.x[co + c] = xn;
       bad |= !isfinite(xn);
-      if (improve) vec.xbest[co + c] = xn;
+      if (improve) vec.xbest[co + c] = mon ? xo : xn;
       wss += wc * wc;
     }
     if (bad) atomicOr(&s_bad, 1);
@@ -252,12 +255,13 @@ __global__ void __launch_bounds__(NT) lsqr_qtu_kernel(fl_blockop op, fl_lsqr_vec
   if (threadIdx.x != 0) return;
   *op.counter = 0u;
   st->it = it;
+  if (st->monitor) st->improved = 0;
   if (*(volatile int32_t*)&st->nonfinite) {  // DivergenceError("non-finite iterate at iteration it")
     st->diverged_at = it;
     st->done = 1;
     return;
   }
-  if (improve) {
+  if (improve && !st->monitor) {
     st->best = phibar;
     st->best_it = it;
   }
@@ -482,11 +486,12 @@ extern "C" int fl_lsqr_init(const fl_blockop* op, const double* rhs, fl_lsqr_vec
   return FL_OK;
 }
 
-extern "C" int fl_lsqr_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t first_it,
-                               int64_t count, void* stream) {
+extern "C" int fl_lsqr_iterate_monitored(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st,
+                                         int64_t first_it, int64_t count, const fl_test_monitor* mon,
+                                         void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (op->n_col_tiles == 0 || op->n_row_tiles == 0) return FL_ERR_INVALID;
-  if (use_fused(op)) return fl::lsqr_fused_iterate(op, vecs, st, first_it, count, s);
+  if (use_fused(op)) return fl::lsqr_fused_iterate(op, vecs, st, first_it, count, mon, s);
   int e = set_smem((const void*)lsqr_qv_kernel, col_smem(op));
   if (e) return e;
   e = set_smem((const void*)lsqr_qtu_kernel, row_smem(op));
@@ -496,9 +501,15 @@ extern "C" int fl_lsqr_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr
     lsqr_qv_kernel<<<op->n_row_tiles, NT, col_smem(op), s>>>(*op, *vecs, st);
     lsqr_ured_kernel<<<grid_rows(op), NT, 0, s>>>(*op, *vecs, st, it);
     lsqr_qtu_kernel<<<op->n_col_tiles, NT, row_smem(op), s>>>(*op, *vecs, st, it);
+    if (mon && (e = fl::monitor_step(mon, vecs->x, st, it, s))) return e;
   }
   FL_CHECK_LAUNCH();
   return FL_OK;
+}
+
+extern "C" int fl_lsqr_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t first_it,
+                               int64_t count, void* stream) {
+  return fl_lsqr_iterate_monitored(op, vecs, st, first_it, count, nullptr, stream);
 }
 
 extern "C" int fl_backsub_scatter(int32_t nblocks, int32_t K, const double* R, const int32_t* rank,

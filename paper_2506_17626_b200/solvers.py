@@ -15,9 +15,11 @@ iterate at the end). Operator polymorphism follows `as_operator`
 
 Monitor semantics (solvers.py:47-69): without an `error_fn` the device keeps
 the best (lowest-residual) iterate itself and the records are rebuilt from
-the device phibar trace; with an `error_fn` the loop is run in chunks of
-`stride` iterations and x is copied back at each recorded iteration to call
-it. Keyword-only `atol`/`btol`/`conlim` add scipy's stopping rule (SURVEY.md
+the device phibar trace; with a `monitor.DeviceL1Error` (the runner's
+test-lattice error) the error of every recorded iterate is evaluated inside
+the device loop (K6) and the best iterate is kept on the device; with any
+other `error_fn` the loop is run in chunks of `stride` iterations and x is
+copied back at each recorded iteration to call it. Keyword-only `atol`/`btol`/`conlim` add scipy's stopping rule (SURVEY.md
 §0 F2); the default is the reference behaviour, a fixed budget.
 """
 
@@ -158,11 +160,13 @@ class DeviceLsqr:
         self.vecs = _lib.LsqrVecs(*(D.ptr(a) for a in (self.u, self.v, self.vp, self.w, self.x,
                                                           self.xbest, self.trace)))
 
-    def reset_state(self, stride: int, track_best: bool, atol=None, btol=None, conlim=1e8):
+    def reset_state(self, stride: int, track_best: bool, atol=None, btol=None, conlim=1e8,
+                    monitor: bool = False):
         st = _lib.LsqrState()
         st.best = np.inf if track_best else -np.inf
         st.best_it = -1
         st.stride = max(int(stride), 1)
+        st.monitor = 1 if monitor else 0
         if atol is not None or btol is not None:
             st.use_rule = 1
             st.atol = float(atol or 0.0)
@@ -181,12 +185,24 @@ class DeviceLsqr:
                                   C.byref(self.vecs), D.ptr(self.state), D.stream_ptr()),
                    "fl_lsqr_init")
 
-    def iterate(self, first_it: int, count: int):
+    def iterate(self, first_it: int, count: int, monitor=None):
+        """Enqueue iterations first_it..first_it+count-1; `monitor` = a
+        `_lib.TestMonitor` evaluated after every recorded iteration (K6)."""
         if count <= 0:
             return
-        _lib.check(_lib.lib().fl_lsqr_iterate(C.byref(self.blocks.struct()), C.byref(self.vecs),
-                                              D.ptr(self.state), int(first_it), int(count),
-                                              D.stream_ptr()), "fl_lsqr_iterate")
+        L = _lib.lib()
+        if monitor is None:
+            _lib.check(L.fl_lsqr_iterate(C.byref(self.blocks.struct()), C.byref(self.vecs),
+                                         D.ptr(self.state), int(first_it), int(count),
+                                         D.stream_ptr()), "fl_lsqr_iterate")
+            return
+        _lib.check(L.fl_lsqr_iterate_monitored(C.byref(self.blocks.struct()), C.byref(self.vecs),
+                                               D.ptr(self.state), int(first_it), int(count),
+                                               C.byref(monitor), D.stream_ptr()),
+                   "fl_lsqr_iterate_monitored")
+        _lib.check(L.fl_lsqr_monitor_flush(C.byref(self.blocks.struct()), C.byref(self.vecs),
+                                           D.ptr(self.state), D.stream_ptr()),
+                   "fl_lsqr_monitor_flush")
 
 
 def lsqr(operator, rhs: np.ndarray, max_iters: int,
@@ -202,9 +218,14 @@ def lsqr(operator, rhs: np.ndarray, max_iters: int,
     max_iters = int(max_iters)
     n = int(shape[1])
     run = DeviceLsqr(blocks, max_iters)
-    host_error = monitor.error_fn is not None
+    from .monitor import DeviceL1Error
+    dev_error = isinstance(monitor.error_fn, DeviceL1Error)
+    if dev_error and monitor.error_fn.n != n:
+        raise InvalidInputError(f"error function expects iterates of length {monitor.error_fn.n}, "
+                                f"operator has {n} columns")
+    host_error = monitor.error_fn is not None and not dev_error
     run.reset_state(monitor.stride, track_best=not host_error, atol=atol, btol=btol,
-                    conlim=conlim)
+                    conlim=conlim, monitor=dev_error)
     run.init(D.to_dev(rhs))
     st = run.read_state()
     x0 = np.zeros(n)
@@ -215,7 +236,13 @@ def lsqr(operator, rhs: np.ndarray, max_iters: int,
         monitor.observe(0, x0, lambda: st.beta)
         return SolveResult(x0, 0, st.beta, monitor, breakdown=True)
 
-    if not host_error:
+    if dev_error:
+        err_trace = D.torch().full((max_iters + 2,), float("nan"), dtype=D.torch().float64,
+                                   device=run.x.device)
+        mon = monitor.error_fn.struct(err_trace)
+        run.iterate(1, max_iters, mon)
+        st = run.read_state()
+    elif not host_error:
         run.iterate(1, max_iters)
         st = run.read_state()
     else:
@@ -241,11 +268,12 @@ def lsqr(operator, rhs: np.ndarray, max_iters: int,
     x = D.to_host(run.x)[:n]
     if not host_error:
         trace = D.to_host(run.trace)
+        errs = D.to_host(err_trace) if dev_error else trace
         stride = max(monitor.stride, 1)
         for it in range(1, iters + 1):
             if stride > 1 and it % stride != 0:
                 continue
-            monitor.records.append((it, float(trace[it]), float(trace[it])))
+            monitor.records.append((it, float(trace[it]), float(errs[it])))
         if st.best_it >= 1:
             monitor.best_error = float(st.best)
             monitor.best_iteration = int(st.best_it)

@@ -177,7 +177,60 @@ def demo_report_golden():
         json.dump(keep, fh, indent=1)
 
 
+def masked_golden():
+    """Hard-constrained problems through the reference: the laplace demo
+    config (pkg/demos/out/laplace/laplace-multiscale, seed 0) and a small
+    wave problem (mask x ramp plus Gaussian-pulse lift): assembly digests,
+    rhs, two full blocks, and P c + lift at the test points for a fixed c."""
+    import json
+    cases = {
+        "laplace": (r_prob.laplace_problem(3), 16, 2.9, 16, None),
+        "wave": (r_prob.wave_problem(0.4), 4, 2.9, 8, None),
+    }
+    for name, (prob, S, ov, K, ipd) in cases.items():
+        dec = r_dom.decompose(prob.domain, S, ov)
+        basis = r_basis.init_basis(dec, K, 1, "tanh", r_lin.RandomSource(0).generator())
+        system = r_asm.assemble(prob, dec, basis, interior_per_dim=ipd)
+        if name == "laplace":
+            ts = r_asm.make_test_set(prob, dec)
+            pts = ts.points
+        else:
+            rng = np.random.default_rng(5)
+            pts = np.column_stack([rng.uniform(-0.95, 0.95, (600, 2)), rng.uniform(0.02, 0.98, 600)])
+        phi, lift = r_asm.solution_matrix(prob, dec, basis, pts)
+        c = np.random.default_rng(7).standard_normal(basis.column_count)
+        full = (0, len(system.blocks) // 2)
+        np.savez_compressed(
+            os.path.join(HERE, f"masked_{name}.npz"),
+            w=basis.weights[0], b=basis.biases[0], rhs=system.rhs, axes=np.concatenate(system.lattice_axes),
+            row_count=system.row_count, column_count=system.column_count,
+            block_rows_len=np.array([b.rows.size for b in system.blocks]),
+            block_rows=np.concatenate([b.rows for b in system.blocks]),
+            block_digest=np.stack([block_digest(b.matrix) for b in system.blocks]),
+            full_idx=np.array(full), full0=system.blocks[full[0]].matrix, full1=system.blocks[full[1]].matrix,
+            points=pts, pc=phi @ c, lift=lift, c=c, phi_nnz=phi.nnz,
+            phi_digest=np.array([phi.data.sum(), np.abs(phi.data).sum(), (phi.data ** 2).sum()]))
+    src = os.path.join(os.path.dirname(os.path.dirname(featlsq.__file__)), "..", "demos",
+                       "out", "laplace", "laplace-multiscale", "report.json")
+    with open(src) as fh:
+        rep = json.load(fh)
+    keep = dict(rows=rep["rows"], columns=rep["columns"], kept=rep["kept"],
+                test_points=rep["test_points"],
+                config={k: rep["config"][k] for k in
+                        ("scale_count", "count_per_dim", "overlap", "features", "sigma",
+                         "max_iters", "seeds", "eval_stride")},
+                seeds=[{k: s[k] for k in ("seed", "error", "best_iteration", "iterations_run",
+                                          "residual_norm", "drop_fraction")}
+                       for s in rep["seeds"]])
+    with open(os.path.join(HERE, "laplace_report.json"), "w") as fh:
+        json.dump(keep, fh, indent=1)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["masked"]:
+        masked_golden()
+        sys.exit(0)
+    masked_golden()
     demo_report_golden()
     print("reference featlsq", featlsq.__version__, "from", featlsq.__file__)
     for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):

@@ -43,14 +43,16 @@ def _struct_fields(name):
         decl = decl.strip()
         if not decl:
             continue
-        names += [piece.replace("*", " ").split()[-1] for piece in decl.split(",")]
+        names += [re.sub(r"\[.*\]", "", piece.replace("*", " ").split()[-1])
+                  for piece in decl.split(",")]
     return names
 
 
 @pytest.mark.parametrize("cname,pyname", [("fl_blockop", "BlockOp"),
                                           ("fl_assembly_desc", "AssemblyDesc"),
                                           ("fl_lsqr_state", "LsqrState"),
-                                          ("fl_lsqr_vecs", "LsqrVecs")])
+                                          ("fl_lsqr_vecs", "LsqrVecs"),
+                                          ("fl_test_monitor", "TestMonitor")])
 def test_ctypes_structs_match_header(cname, pyname):
     py = getattr(_lib, pyname)
     assert [f[0] for f in py._fields_] == _struct_fields(cname)
