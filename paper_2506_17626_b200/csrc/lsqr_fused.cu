@@ -24,11 +24,12 @@
 // One CTA streams one column range of one block: block j's column tiles are
 // split over S CTAs (S <= FL_LSQR_SPLIT_MAX), each writing its own copy of
 // p_j, which the row kernel sums in a fixed order — finer work units shorten
-// the tail of the last wave. The CTA shape (NT threads, RPT rows per thread,
+// the tail of the last wave. The CTA shape (NT threads, RP row pairs per thread,
 // W columns per tile, ST ring stages) is picked per layout from the
 // instantiated table at the bottom: NT = 256 runs two CTAs per SM so one
 // block's prologue/epilogue overlaps another block's stream.
 #include <float.h>
+#include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -42,20 +43,46 @@ constexpr int smem_per_cta(int mb) { return mb <= 1 ? 232448 : (233472 - mb * 10
 
 __device__ __forceinline__ bool is_done(const fl_lsqr_state* st) { return *(volatile const int32_t*)&st->done; }
 
+// Warp sums of W per-lane values with a butterfly: the first log2(W) steps
+// halve the set of live columns per lane group, so W columns cost
+// 5 shuffles in total; returns in lane (32/W) c the total of column c.
+template <int W>
+__device__ __forceinline__ double warp_sums(const double (&a)[W], int lane) {
+  double v[W];
+#pragma unroll
+  for (int c = 0; c < W; ++c) v[c] = a[c];
+#pragma unroll
+  for (int half = W / 2, o = 16; half >= 1; half /= 2, o /= 2) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int c = 0; c < half; ++c) {
+      const double send = up ? v[c] : v[c + half];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+      v[c] = (up ? v[c + half] : v[c]) + recv;
+    }
+  }
+  double s = v[0];
+#pragma unroll
+  for (int o = 32 / W / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 // mode 0: initialisation (v = 0, no x update); mode 1: iteration `it`.
-// RPT * NT >= ld of every block.
-template <int NT, int RPT, int W, int ST, int MB>
+// RP row pairs per thread: 2 * RP * NT >= ld of every block. W columns are
+// reduced together per barrier; the ring holds SL single-column slots
+// (SL >= 2W) so SL - W columns stream in while a tile is being used.
+template <int NT, int RP, int W, int SL, int MB>
 __global__ void __launch_bounds__(NT, MB)
     fused_kernel(fl_blockop op, fl_lsqr_vecs vec, fl_lsqr_state* st, int64_t it, int mode, int ldmax, int S) {
   constexpr int NW = NT / 32;
-  constexpr int GL = NW;        // lanes per column in the cross-warp shuffle tree
-  constexpr int CPP = 32 / GL;  // columns per shuffle pass
+  constexpr bool KEEP = RP * W <= 6;  // tile values stay in registers between the two products
+  static_assert(SL >= 2 * W, "ring too shallow");
   if (is_done(st)) return;
   extern __shared__ __align__(128) double sm[];
-  double* tile = sm;  // [ST][W][ldmax] column tiles of Q_j
-  __shared__ double red[2 * NW * W];
+  double* ring = sm;  // [SL][ldmax] columns of Q_j
+  __shared__ __align__(16) double red[2 * NW * W];
   __shared__ double red2[NW];
-  __shared__ __align__(8) uint64_t bars[ST];
+  __shared__ __align__(8) uint64_t bars[SL];
   __shared__ int s_bad;
   __shared__ bool is_last;
 
@@ -72,41 +99,36 @@ __global__ void __launch_bounds__(NT, MB)
   const int nt_all = (nc + W - 1) / W;
   const int t0 = (int)((int64_t)nt_all * h / S);  // this CTA's column tiles [t0, t1)
   const int t1 = (int)((int64_t)nt_all * (h + 1) / S);
-  const int ntiles = work ? t1 - t0 : 0;
   const int cbeg = min(t0 * W, nc), cend = min(t1 * W, nc);  // x update runs even when beta = 0
   const int64_t cob = co + cbeg;  // first y-space entry of the range
   const int ncr = cend - cbeg;
+  const int ncw = work ? ncr : 0;  // columns streamed
+  const int ntiles = (ncw + W - 1) / W;
   if (threadIdx.x == 0) {
     s_bad = 0;
-    for (int s = 0; s < ST; ++s)
+    for (int s = 0; s < SL; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bars[s]))
                    : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  // TMA bulk copies: thread 0 moves whole columns (ld * 8 bytes each) into
-  // the stage and arms the stage's mbarrier with the byte count
-  auto issue = [&](int tidx) {
-    if (threadIdx.x != 0 || tidx >= ntiles) return;
-    const int s = tidx % ST;
-    const int c0 = (t0 + tidx) * W;
-    const int ncl = min(W, nc - c0);
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[s]);
+  // TMA bulk copy of local column k (ld * 8 bytes) into slot k % SL, armed
+  // on that slot's mbarrier (thread 0)
+  auto issue = [&](int k) {
+    if (threadIdx.x != 0 || k >= ncw) return;
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[k % SL]);
     const unsigned bytes = (unsigned)ld * 8u;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes * ncl) : "memory");
-    for (int c = 0; c < ncl; ++c) {
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + (s * W + c) * ldmax);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-          "l"(Q + (int64_t)(c0 + c) * ld), "r"(bytes), "r"(bar)
-          : "memory");
-    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (k % SL) * ldmax);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(Q + (int64_t)(cbeg + k) * ld), "r"(bytes), "r"(bar)
+                 : "memory");
   };
-  auto wait_tile = [&](int tidx) {
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[tidx % ST]);
-    const unsigned parity = (unsigned)((tidx / ST) & 1);
+  auto wait_col = [&](int k) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[k % SL]);
+    const unsigned parity = (unsigned)((k / SL) & 1);
     unsigned ok = 0;
     while (!ok)
       asm volatile(
@@ -116,8 +138,7 @@ __global__ void __launch_bounds__(NT, MB)
           : "memory");
   };
   // the ring fills while the x update and the u gather run
-#pragma unroll
-  for (int s = 0; s < ST - 1; ++s) issue(s);
+  for (int k = 0; k < SL - W; ++k) issue(k);
 
   // ---- x update for this block's columns (iteration `it`) ----
   double wss = 0.0;
@@ -148,22 +169,23 @@ __global__ void __launch_bounds__(NT, MB)
   double ass = 0.0;  // sum of v'^2 over this CTA's columns (thread 0)
   if (work) {
     // ---- u'/beta and the partial product live in registers: thread t owns
-    //      rows t, t + NT, ... ----
+    //      the row pairs (2t, 2t+1) + 2 NT k, read as 16-byte shared loads ----
     const int32_t* rows = op.rows + op.row_off[j];
-    double uh_r[RPT], pp_r[RPT];
+    double2 uh_r[RP], pp_r[RP];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = threadIdx.x + i * NT;
-      uh_r[i] = (r < m) ? vec.u[rows[r]] / beta : 0.0;
-      pp_r[i] = 0.0;
+    for (int i = 0; i < RP; ++i) {
+      const int r = 2 * (threadIdx.x + i * NT);
+      uh_r[i].x = (r < m) ? vec.u[rows[r]] / beta : 0.0;
+      uh_r[i].y = (r + 1 < m) ? vec.u[rows[r + 1]] / beta : 0.0;
+      pp_r[i] = make_double2(0.0, 0.0);
     }
     // v_j[tile] is read one tile ahead (broadcast loads, off the critical path)
     double vnext[W];
     auto load_v = [&](int tdx) {
 #pragma unroll
       for (int c = 0; c < W; ++c) {
-        const int col = (t0 + tdx) * W + c;
-        vnext[c] = (mode == 1 && col < nc) ? vec.v[co + col] : 0.0;
+        const int col = cbeg + tdx * W + c;
+        vnext[c] = (mode == 1 && col < cend) ? vec.v[co + col] : 0.0;
       }
     };
     load_v(0);
@@ -172,71 +194,77 @@ __global__ void __launch_bounds__(NT, MB)
 #pragma unroll
       for (int c = 0; c < W; ++c) vcur[c] = vnext[c];
       if (tdx + 1 < ntiles) load_v(tdx + 1);
-      wait_tile(tdx);
-      const int ncl = min(W, nc - (t0 + tdx) * W);  // valid columns in this tile
-      const double* tl = tile + (tdx % ST) * W * ldmax;
+      const int k0 = tdx * W;
+      const int ncl = min(W, ncw - k0);  // valid columns in this tile
+      const double* cp[W];
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        if (c < ncl) wait_col(k0 + c);
+        cp[c] = ring + ((k0 + c) % SL) * ldmax;
+      }
+      double2 q[KEEP ? RP : 1][W];
       double acc[W];
 #pragma unroll
       for (int c = 0; c < W; ++c) acc[c] = 0.0;
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int r = threadIdx.x + i * NT;
-        if (r < ld) {
+      for (int i = 0; i < RP; ++i) {
+        const int r = 2 * (threadIdx.x + i * NT);
 #pragma unroll
-          for (int c = 0; c < W; ++c)
-            if (c < ncl) acc[c] += tl[c * ldmax + r] * uh_r[i];
+        for (int c = 0; c < W; ++c) {
+          const double2 x = (r < ld && c < ncl) ? *reinterpret_cast<const double2*>(cp[c] + r)
+                                                : make_double2(0.0, 0.0);
+          if (KEEP) q[KEEP ? i : 0][c] = x;
+          acc[c] += x.x * uh_r[i].x + x.y * uh_r[i].y;
         }
       }
-#pragma unroll
-      for (int c = 0; c < W; ++c) {
-        const double s = fl::warp_sum(acc[c]);
-        if (lane == 0) red[(tdx & 1) * NW * W + wid * W + c] = s;
+      double* rw = red + (tdx & 1) * NW * W;  // [c][warp]
+      {
+        const double s = warp_sums<W>(acc, lane);
+        if ((lane & (32 / W - 1)) == 0) rw[(lane / (32 / W)) * NW + wid] = s;
       }
-      __syncthreads();         // partials visible; every thread is done with tile tdx-1
-      issue(tdx + ST - 1);     // refills the stage tile tdx-1 used
-      // v'[tile] = Q[:, tile]^T u - beta v[tile] (solvers.py:136): every warp
-      // sums the NW warp partials itself with the same GL-lane shuffle tree
-      // (CPP columns per pass), so no second barrier is needed; `red`
-      // alternates buffers by tile parity
+      __syncthreads();  // partials visible; every thread is done with tile tdx-1
+      for (int k = SL - W + k0; k < SL + k0; ++k) issue(k);  // refill tile tdx-1's slots
+      // v'[tile] = Q[:, tile]^T u - beta v[tile] (solvers.py:136): every thread
+      // sums the NW warp partials itself in warp order (broadcast 16-byte
+      // loads), so no second barrier is needed; `red` alternates by parity
       double tc[W];
-      const double* rb = red + (tdx & 1) * NW * W;
-#pragma unroll
-      for (int c0 = 0; c0 < W; c0 += CPP) {
-        const int c = c0 + lane / GL;
-        double s = (c < W) ? rb[(lane % GL) * W + c] : 0.0;
-#pragma unroll
-        for (int o = GL / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-#pragma unroll
-        for (int q = 0; q < CPP; ++q) {
-          const double sq = __shfl_sync(0xffffffffu, s, q * GL);
-          if (c0 + q < W) tc[c0 + q] = sq;
-        }
-      }
 #pragma unroll
       for (int c = 0; c < W; ++c) {
-        const int col = (t0 + tdx) * W + c;
+        const double2* rp = reinterpret_cast<const double2*>(rw + c * NW);
+        double s = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < NW / 2; ++w2) {
+          const double2 pr = rp[w2];
+          s += pr.x;
+          s += pr.y;
+        }
         double vn = 0.0;
-        if (c < ncl) vn = tc[c] - ((mode == 1) ? beta * vcur[c] : 0.0);
+        if (c < ncl) vn = s - ((mode == 1) ? beta * vcur[c] : 0.0);
         tc[c] = vn;
         if (threadIdx.x == 0) {
-          if (c < ncl) vec.vp[co + col] = vn;
+          if (c < ncl) vec.vp[cob + k0 + c] = vn;
           ass += vn * vn;
         }
       }
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int r = threadIdx.x + i * NT;
-        if (r < ld) {
+      for (int i = 0; i < RP; ++i) {
+        const int r = 2 * (threadIdx.x + i * NT);
 #pragma unroll
-          for (int c = 0; c < W; ++c)
-            if (c < ncl) pp_r[i] += tl[c * ldmax + r] * tc[c];
+        for (int c = 0; c < W; ++c) {
+          const double2 x = KEEP ? q[KEEP ? i : 0][c]
+                                 : ((r < ld && c < ncl) ? *reinterpret_cast<const double2*>(cp[c] + r)
+                                                        : make_double2(0.0, 0.0));
+          pp_r[i].x += x.x * tc[c];
+          pp_r[i].y += x.y * tc[c];
         }
       }
     }
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = threadIdx.x + i * NT;
-      if (r < m) op.partial[h * op.partial_len + op.row_off[j] + r] = pp_r[i];
+    for (int i = 0; i < RP; ++i) {
+      const int r = 2 * (threadIdx.x + i * NT);
+      double* pout = op.partial + h * op.partial_len + op.row_off[j];
+      if (r < m) pout[r] = pp_r[i].x;
+      if (r + 1 < m) pout[r + 1] = pp_r[i].y;
     }
   }
   // ---- grid reductions: alpha^2, w^2, non-finite ----
@@ -390,50 +418,51 @@ __global__ void __launch_bounds__(256) row_kernel(fl_blockop op, fl_lsqr_vecs ve
 }
 
 // ---- CTA-shape table -----------------------------------------------------
-// A shape fits a layout when RPT * NT >= ldmax and its ring (ST * W * ldmax
+// A shape fits a layout when 2 * RP * NT >= ldmax and its ring (ST * ldmax
 // doubles) plus static shared memory fits the per-CTA budget. Entries are in
 // preference order; FEATLSQ_FUSED="NT,W,ST,MB" restricts the choice (tuning).
 
 enum { SKIP = 1 };
 
-template <int NT, int RPT, int W, int ST, int MB>
+template <int NT, int RP, int W, int ST, int MB>
 int try_fused(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t it, int mode, int ldmax,
               int S, cudaStream_t s, bool dry) {
-  if ((int64_t)RPT * NT < ldmax) return SKIP;
+  if ((int64_t)2 * RP * NT < ldmax) return SKIP;
   static int stat = -1;
   static size_t attr = 0;
   if (stat < 0) {
     cudaFuncAttributes a;
-    FL_CUDA(cudaFuncGetAttributes(&a, fused_kernel<NT, RPT, W, ST, MB>));
+    FL_CUDA(cudaFuncGetAttributes(&a, fused_kernel<NT, RP, W, ST, MB>));
     stat = (int)a.sharedSizeBytes;
   }
-  const size_t dyn = (size_t)ST * W * ldmax * sizeof(double);
+  const size_t dyn = (size_t)ST * ldmax * sizeof(double);
   if (dyn + stat > (size_t)smem_per_cta(MB)) return SKIP;
   if (dry) return FL_OK;
   if (dyn > attr) {
-    FL_CUDA(cudaFuncSetAttribute(fused_kernel<NT, RPT, W, ST, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FL_CUDA(cudaFuncSetAttribute(fused_kernel<NT, RP, W, ST, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dyn));
     attr = dyn;
   }
-  fused_kernel<NT, RPT, W, ST, MB><<<op->nblocks * S, NT, dyn, s>>>(*op, *vecs, st, it, mode, ldmax, S);
+  fused_kernel<NT, RP, W, ST, MB><<<op->nblocks * S, NT, dyn, s>>>(*op, *vecs, st, it, mode, ldmax, S);
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
 
 struct Shape {
-  int nt, rpt, w, st, mb;
+  int nt, rp, w, st, mb;
   int (*fn)(const fl_blockop*, fl_lsqr_vecs*, fl_lsqr_state*, int64_t, int, int, int, cudaStream_t, bool);
 };
 
 #define FL_SHAPE(NT, R, W, S, MB) {NT, R, W, S, MB, try_fused<NT, R, W, S, MB>}
 const Shape kShapes[] = {
-    FL_SHAPE(512, 1, 8, 3, 1), FL_SHAPE(512, 2, 8, 3, 1), FL_SHAPE(512, 3, 4, 3, 1), FL_SHAPE(512, 3, 3, 3, 1),
-    FL_SHAPE(512, 4, 4, 3, 1), FL_SHAPE(512, 4, 3, 3, 1), FL_SHAPE(512, 4, 2, 4, 1),
-    FL_SHAPE(256, 12, 1, 3, 3), FL_SHAPE(256, 12, 1, 5, 2), FL_SHAPE(256, 12, 1, 4, 2),
-    FL_SHAPE(128, 24, 1, 3, 3), FL_SHAPE(128, 24, 1, 2, 4), FL_SHAPE(256, 12, 1, 2, 4),
-    FL_SHAPE(512, 6, 3, 3, 1), FL_SHAPE(512, 6, 1, 9, 1),
-    FL_SHAPE(512, 8, 2, 3, 1), FL_SHAPE(512, 8, 1, 6, 1), FL_SHAPE(512, 8, 1, 4, 1),
-    FL_SHAPE(512, 12, 1, 4, 1), FL_SHAPE(512, 12, 1, 3, 1),
+    // ld <= 1024 / 2048: one 512-thread CTA per SM, several columns per barrier
+    FL_SHAPE(512, 1, 8, 24, 1), FL_SHAPE(512, 2, 4, 12, 1), FL_SHAPE(512, 2, 2, 8, 1),
+    // ld <= 3072 (cfg3, cfg4): two 256-thread CTAs per SM, one column per barrier
+    // (measured on cfg4: 1.436 ms/it vs 1.52 for 384 threads, 1.90 for 512)
+    FL_SHAPE(256, 6, 1, 4, 2), FL_SHAPE(256, 6, 1, 5, 2), FL_SHAPE(256, 6, 1, 3, 3),
+    // ld <= 6144 (cfg5): one 512-thread CTA per SM
+    FL_SHAPE(512, 4, 1, 6, 1), FL_SHAPE(512, 4, 1, 4, 1),
+    FL_SHAPE(512, 6, 1, 4, 1), FL_SHAPE(512, 6, 1, 3, 1),
 };
 #undef FL_SHAPE
 
@@ -447,8 +476,10 @@ struct EnvShape {
 
 int ldmax_of(const fl_blockop* op) { return (int)fl::round_up(op->max_rows > 0 ? op->max_rows : 1, 16); }
 
-// Column split S: the fewest CTAs per block that give at least 4 work units
-// per resident CTA slot (FEATLSQ_SPLIT overrides, tuning).
+// Column split S: maximise the last-wave occupancy of J*S work units over
+// the resident CTA slots, with a small penalty per extra split (every split
+// re-gathers u and writes its own partial copy). Measured: cfg3 (J = 256)
+// S = 1, cfg4/cfg5 (J = 1024 / 512) S = 2. FEATLSQ_SPLIT overrides (tuning).
 int split_of(const fl_blockop* op, const Shape& sh) {
   static const int env = [] {
     const char* e = getenv("FEATLSQ_SPLIT");
@@ -462,9 +493,18 @@ int split_of(const fl_blockop* op, const Shape& sh) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  int S = 1;
-  while (S < FL_LSQR_SPLIT_MAX && (int64_t)op->nblocks * S < 4LL * nsm * sh.mb) ++S;
-  return S;
+  const double slots = (double)nsm * sh.mb;
+  int best = 1;
+  double best_score = -1.0;
+  for (int S = 1; S <= FL_LSQR_SPLIT_MAX; ++S) {
+    const double waves = (double)op->nblocks * S / slots;
+    const double score = waves / ceil(waves) - 0.02 * (S - 1);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = S;
+    }
+  }
+  return best;
 }
 
 // the shape picked for this layout (first fit in table order), or nullptr

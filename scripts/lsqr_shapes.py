@@ -48,3 +48,26 @@ out = dict(shape=os.environ.get("FEATLSQ_FUSED", "default"), ms_per_iter=round(m
            GBs_Q=round(8 * nnz / ms / 1e6, 1), GBs_store_sum=round(8 * vals.numel() / ms_read / 1e6, 1),
            phibar=st.phibar, it=st.it, done=st.done)
 print(json.dumps(out))
+
+# CUDA-graph replay of the same iterations (launch gaps)
+if os.environ.get("FEATLSQ_GRAPH"):
+    solver.reset_state(1, False)
+    solver.init(rhs)
+    solver.iterate(1, 10)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            solver.iterate(11, 50)
+    torch.cuda.synchronize()
+    solver.reset_state(1, False)
+    solver.init(rhs)
+    solver.iterate(1, 10)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(its // 50):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print(json.dumps(dict(graph_ms_per_iter=round(e0.elapsed_time(e1) / (its // 50 * 50), 4))))
