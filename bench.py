@@ -177,11 +177,10 @@ def product(args, rank, world, local_rank):
     from paper_2506_17626_b200.filtering import recover_solution_device
     from paper_2506_17626_b200.solvers import DeviceLsqr
 
+    from paper_2506_17626_b200.replicas import (barrier, max_over_ranks, replica_seed,
+                                                 whole_job_rate)
     torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-    wl = workloads.build(args.config, seed=rank)
+    wl = workloads.build(args.config, seed=replica_seed(rank))
     iters = args.lsqr_iters
 
     # ---- device-resident pipeline: host preparation outside the timed region
@@ -218,8 +217,7 @@ def product(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step(events())
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    barrier()
     clocks = Clocks(local_rank)
     clocks.start()
     torch.cuda.synchronize()
@@ -231,12 +229,8 @@ def product(args, rank, world, local_rank):
     t_end.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    elapsed = t_start.elapsed_time(t_end) / 1e3
-    if dist:
-        tt = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
-        dist.barrier()
+    elapsed = max_over_ranks(t_start.elapsed_time(t_end) / 1e3)
+    barrier()
 
     def avg(a, b):
         return float(np.mean([e[a].elapsed_time(e[b]) for e in evs])) / 1e3
@@ -266,7 +260,7 @@ def product(args, rank, world, local_rank):
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(args.config, {}).get("lsqr_bytes_per_iter")
     out = {
-        "metric": METRIC, "value": round(world / step_s, 6), "unit": UNIT,
+        "metric": METRIC, "value": round(whole_job_rate(world, 1, step_s), 6), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -313,8 +307,7 @@ def product(args, rank, world, local_rank):
             return fl.recover_solution(fs_h, res.solution)
         e2e_step()
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+        barrier()
         x0 = dict(D.XFER)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -322,12 +315,8 @@ def product(args, rank, world, local_rank):
             e2e_step()
         e1.record()
         torch.cuda.synchronize()
-        t_e2e = e0.elapsed_time(e1) / 1e3
-        if dist:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
-        out["e2e"] = {"value": round(world * fl_steps / t_e2e, 6), "unit": UNIT,
+        t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        out["e2e"] = {"value": round(whole_job_rate(world, fl_steps, t_e2e), 6), "unit": UNIT,
                       "h2d_bytes_per_step": int((D.XFER["h2d"] - x0["h2d"]) / fl_steps),
                       "d2h_bytes_per_step": int((D.XFER["d2h"] - x0["d2h"]) / fl_steps),
                       "ms_per_step": round(t_e2e / fl_steps * 1e3, 2)}
