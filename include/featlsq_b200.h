@@ -238,6 +238,52 @@ int fl_lsqr_iterate_monitored(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_
 int fl_lsqr_monitor_flush(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, void* stream);
 
 /* ------------------------------------------------------------------------
+ * N4 — CG on the normal equations with an optional block (additive-Schwarz)
+ * preconditioner (solvers.py:150-239). Loop control reuses fl_lsqr_state
+ * (it, done, breakdown, stride, best / best_it / improved, diverged_at;
+ * monitor must be 1); scalars: alpha = r.z, beta = p.q, phi = step,
+ * theta = r.z_next / r.z, phibar = last recorded residual ||M x - rhs||.
+ * ---------------------------------------------------------------------- */
+typedef struct fl_cg_vecs {
+  double* tmp;              /* (N,) M p / M x */
+  double* p;                /* (n,) */
+  double* q;                /* (n,) M^T M p */
+  double* r;                /* (n,) normal-equation residual */
+  double* z;                /* (n,) P r (may equal r: no preconditioner) */
+  double* x;                /* (n,) */
+  double* xbest;            /* (n,) best recorded iterate */
+  double* res_trace;        /* (max_iters + 1,) residual per recorded iteration */
+  const double* rhs;        /* (N,) */
+  double* scratch;          /* (>= 2 * 592) reduction slots */
+  unsigned int* counter;    /* (1,) zero-initialised */
+  int32_t stride;           /* recorded iterations: it % stride == 0 */
+} fl_cg_vecs;
+
+/* z[idx_b] = inv_b r[idx_b], inv_b row-major size_b x size_b with
+ * size_b = idx_off[b+1] - idx_off[b] */
+typedef struct fl_block_precond {
+  int32_t nblocks;
+  int32_t max_size;
+  const int64_t* idx_off;   /* (nblocks + 1,) */
+  const int32_t* idx;       /* concatenated column indices */
+  const int64_t* val_off;   /* (nblocks,) start of inv_b in vals */
+  const double* vals;
+} fl_block_precond;
+
+/* z = P r on its own (AdditiveSchwarz.apply) */
+int fl_block_precond_apply(const fl_block_precond* pre, const double* r, double* z, void* stream);
+/* r = M^T rhs, z = P r, p = z, r.z (pre may be NULL) */
+int fl_cg_init(const fl_blockop* op, fl_cg_vecs* v, const fl_block_precond* pre,
+               fl_lsqr_state* st, void* stream);
+/* iterations first_it .. first_it+count-1; mon (may be NULL) ranks the
+ * recorded iterates by test error instead of residual */
+int fl_cg_iterate(const fl_blockop* op, fl_cg_vecs* v, const fl_block_precond* pre,
+                  fl_lsqr_state* st, int64_t first_it, int64_t count,
+                  const fl_test_monitor* mon, void* stream);
+/* ||M x - rhs|| -> out[0] */
+int fl_cg_residual(const fl_blockop* op, fl_cg_vecs* v, double* out, void* stream);
+
+/* ------------------------------------------------------------------------
  * Recovery (filtering.py:169-183): coeffs[kept global column] = R_j^{-1} y_j,
  * every other entry of coeffs (length J*K) exactly 0.
  * ---------------------------------------------------------------------- */

@@ -534,3 +534,64 @@ def run_rrqr_lsqr(problem, dec, basis, sigma, max_iters, interior_per_dim=None):
     return dict(error=err, best_iteration=best["it"], iterations=its, residual=phibar,
                 drop_fraction=1.0 - off[-1] / sysd["column_count"], kept=int(off[-1]),
                 coeffs=coeffs)
+
+
+# ---------------------------------------------------------------------------
+# N4 baselines (solvers.py:150-239): additive Schwarz, CG on the normal equations
+
+def as_preconditioner(blocks, column_ranges, cutoff=1e-14):
+    """solvers.py:181-192: per block (pseudo-)inverse of A_j^T A_j through
+    numpy's eigh (LAPACK dsyevd, as the reference). Returns (ranges,
+    inverses, degenerate)."""
+    invs, degenerate = [], []
+    for j, mat in enumerate(blocks):
+        gram = mat.T @ mat
+        evals, evecs = np.linalg.eigh(gram)
+        top = float(evals[-1]) if evals.size else 0.0
+        keep = evals > cutoff * top if top > 0.0 else np.zeros_like(evals, dtype=bool)
+        if not keep.all():
+            degenerate.append(j)
+        inv_vals = np.where(keep, 1.0 / np.where(keep, evals, 1.0), 0.0)
+        invs.append((evecs * inv_vals) @ evecs.T)
+    return list(column_ranges), invs, degenerate
+
+
+def as_apply(ranges, invs, vec):
+    out = np.empty_like(vec)
+    for cols, inv in zip(ranges, invs):
+        out[cols] = inv @ vec[cols]
+    return out
+
+
+def cg_normal(matvec, rmatvec, ncols, rhs, max_iters, stride=1, precond=None):
+    """solvers.py:195-239. Returns (x, iterations, final residual, records,
+    breakdown) with records (it, residual, residual) at recorded iterations."""
+    x = np.zeros(ncols)
+    r = rmatvec(rhs)
+    z = precond(r) if precond else r
+    p = z.copy()
+    rz = float(r @ z)
+    records, breakdown, iterations = [], False, 0
+    for it in range(1, max_iters + 1):
+        q = rmatvec(matvec(p))
+        pq = float(p @ q)
+        if pq <= 0.0 or not np.isfinite(pq):
+            breakdown = True
+            break
+        step = rz / pq
+        x = x + step * p
+        r = r - step * q
+        iterations = it
+        if not np.isfinite(x).all():
+            raise DivergenceError(f"non-finite iterate at iteration {it}")
+        if not (stride > 1 and it % stride != 0):
+            res = float(np.linalg.norm(matvec(x) - rhs))
+            records.append((it, res, res))
+        z = precond(r) if precond else r
+        rz_next = float(r @ z)
+        if rz == 0.0:
+            breakdown = True
+            break
+        p = z + (rz_next / rz) * p
+        rz = rz_next
+    return x, iterations, float(np.linalg.norm(matvec(x) - rhs)), records, breakdown

@@ -19,7 +19,8 @@ from .jets import Jet2, radial_jet
 from .monitor import DeviceL1Error, test_error_fn
 from .problems import (ConstraintRows, LinearOperator2, ProblemSpec, laplace_problem,
                        oscillator_problem, wave_problem)
-from .solvers import ConvergenceMonitor, Operator, SolveResult, as_operator, lsqr
+from .solvers import (AdditiveSchwarz, ConvergenceMonitor, Operator, SolveResult, as_operator,
+                      as_preconditioner, cg_normal, lsqr)
 
 __version__ = "0.1.0"
 
@@ -34,5 +35,5 @@ __all__ = [
     "precondition", "qr_column_pivot", "recover_solution",
     "DeviceL1Error", "Jet2", "SolutionBlocks", "TestSet", "evaluate_solution", "l1_error",
     "laplace_problem", "make_test_set", "radial_jet", "solution_matrix", "test_error_fn",
-    "wave_problem",
+    "wave_problem", "AdditiveSchwarz", "as_preconditioner", "cg_normal",
 ]

@@ -70,6 +70,16 @@ class LsqrVecs(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("u", "v", "vp", "w", "x", "xbest", "trace")]
 
 
+class CgVecs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("tmp", "p", "q", "r", "z", "x", "xbest", "res_trace",
+                                          "rhs", "scratch", "counter")] + [("stride", C.c_int32)]
+
+
+class BlockPrecond(C.Structure):
+    _fields_ = [("nblocks", C.c_int32), ("max_size", C.c_int32), ("idx_off", C.c_void_p),
+                ("idx", C.c_void_p), ("val_off", C.c_void_p), ("vals", C.c_void_p)]
+
+
 class TestMonitor(C.Structure):
     _fields_ = [("T", BlockOp), ("lift", C.c_void_p), ("truth", C.c_void_p), ("spread", C.c_double),
                 ("err_trace", C.c_void_p), ("result", C.c_void_p)]
@@ -109,6 +119,11 @@ def lib():
         "fl_lsqr_iterate_monitored": [C.POINTER(BlockOp), C.POINTER(LsqrVecs), vp, C.c_int64,
                                       C.c_int64, C.POINTER(TestMonitor), vp],
         "fl_lsqr_monitor_flush": [C.POINTER(BlockOp), C.POINTER(LsqrVecs), vp, vp],
+        "fl_cg_init": [C.POINTER(BlockOp), C.POINTER(CgVecs), C.POINTER(BlockPrecond), vp, vp],
+        "fl_cg_iterate": [C.POINTER(BlockOp), C.POINTER(CgVecs), C.POINTER(BlockPrecond), vp,
+                          C.c_int64, C.c_int64, C.POINTER(TestMonitor), vp],
+        "fl_cg_residual": [C.POINTER(BlockOp), C.POINTER(CgVecs), vp, vp],
+        "fl_block_precond_apply": [C.POINTER(BlockPrecond), vp, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -128,7 +143,8 @@ EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", 
             "fl_lsqr_iterate", "fl_backsub_scatter", "fl_probe_fp64", "fl_dev_wy_apply",
             "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error",
             "fl_error_blocks", "fl_monitor_error", "fl_lsqr_iterate_monitored",
-            "fl_lsqr_monitor_flush")
+            "fl_lsqr_monitor_flush", "fl_cg_init", "fl_cg_iterate", "fl_cg_residual",
+            "fl_block_precond_apply")
 
 
 def check(code: int, what: str) -> None:

@@ -279,3 +279,207 @@ def lsqr(operator, rhs: np.ndarray, max_iters: int,
             monitor.best_iteration = int(st.best_it)
             monitor.best_iterate = D.to_host(run.xbest)[:n].copy()
     return SolveResult(x, iters, float(st.phibar), monitor, bool(st.breakdown), int(st.istop))
+
+
+# ---------------------------------------------------------------------------
+# N4 baselines: additive Schwarz and CG on the normal equations
+# (solvers.py:150-239; the runner's "cg"/"as-cg" solvers, runner.py:296-305)
+
+class AdditiveSchwarz:
+    """Block-diagonal (pseudo-)inverse of the per-subdomain Gramians
+    (`solvers.py:150-178`). Same fields as the reference; `apply` and the CG
+    loop run the block products on the device (K: `fl_block_precond_apply`).
+    Instances built by `as_preconditioner` keep their inverses on the device
+    and materialise the host tuple on first access."""
+
+    def __init__(self, column_count, block_ranges, block_inverses, degenerate_blocks,
+                 _device=None):
+        self.column_count = int(column_count)
+        self.block_ranges = tuple(np.asarray(r) for r in block_ranges)
+        self._inverses = None if block_inverses is None else tuple(
+            np.asarray(b, dtype=float) for b in block_inverses)
+        self.degenerate_blocks = tuple(int(j) for j in degenerate_blocks)
+        self._dev = _device          # (vals tensor (sum s_b^2,), sizes)
+        self._pre = None
+
+    @property
+    def block_inverses(self) -> tuple:
+        if self._inverses is None:
+            vals = D.to_host(self._dev)
+            out, o = [], 0
+            for r in self.block_ranges:
+                s = r.size
+                out.append(vals[o:o + s * s].reshape(s, s).copy())
+                o += s * s
+            self._inverses = tuple(out)
+        return self._inverses
+
+    def device_struct(self) -> _lib.BlockPrecond:
+        if self._pre is None:
+            sizes = np.array([r.size for r in self.block_ranges], dtype=np.int64)
+            idx_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+            val_off = np.concatenate([[0], np.cumsum(sizes * sizes)[:-1]]).astype(np.int64)
+            idx = (np.concatenate(self.block_ranges).astype(np.int32) if len(sizes)
+                   else np.zeros(0, np.int32))
+            if self._dev is None:
+                self._dev = D.to_dev(np.concatenate([b.ravel() for b in self._inverses])
+                                     if len(sizes) else np.zeros(1))
+            keep = dict(idx_off=D.to_dev(idx_off), idx=D.to_dev(idx), val_off=D.to_dev(val_off))
+            self._keep = keep
+            self._pre = _lib.BlockPrecond(
+                nblocks=len(sizes), max_size=int(sizes.max()) if len(sizes) else 0,
+                idx_off=D.ptr(keep["idx_off"]), idx=D.ptr(keep["idx"]),
+                val_off=D.ptr(keep["val_off"]), vals=D.ptr(self._dev))
+        return self._pre
+
+    def apply(self, vec: np.ndarray) -> np.ndarray:
+        vec = np.asarray(vec, dtype=float)
+        if vec.shape != (self.column_count,):
+            raise InvalidInputError(f"expected shape ({self.column_count},), got {vec.shape}")
+        t = D.torch()
+        r = D.to_dev(vec)
+        z = t.zeros(max(self.column_count, 1), dtype=t.float64, device=r.device)
+        _lib.check(_lib.lib().fl_block_precond_apply(C.byref(self.device_struct()), D.ptr(r),
+                                                     D.ptr(z), D.stream_ptr()),
+                   "fl_block_precond_apply")
+        return D.to_host(z)[:self.column_count]
+
+    def materialize(self) -> np.ndarray:
+        dense = np.zeros((self.column_count, self.column_count))
+        for cols, inv in zip(self.block_ranges, self.block_inverses):
+            dense[np.ix_(cols, cols)] = inv
+        return dense
+
+
+def as_preconditioner(system, cutoff: float = 1e-14) -> AdditiveSchwarz:
+    """`solvers.py:181-192` on the device: Gramians A_j^T A_j from the
+    resident blocks (cuBLAS batched GEMM), eigendecomposition (cuSOLVER),
+    eigenvalues at or below cutoff * largest dropped."""
+    t = D.torch()
+    system.sync_device()
+    st = system.store
+    L = st.layout
+    K = L.K
+    J = L.J
+    grams = t.empty((max(J, 1), K, K), dtype=t.float64, device=st.vals.device)
+    for ldv in np.unique(L.ld):
+        js = np.nonzero(L.ld == ldv)[0]
+        for c0 in range(0, js.size, 64):
+            chunk = js[c0:c0 + 64]
+            # each block's (K, ld) panel is a contiguous slice of the store
+            # (padding rows are exact zeros, so they do not change A^T A)
+            panels = t.stack([st.vals[int(L.off[j]):int(L.off[j]) + K * int(ldv)].view(K, int(ldv))
+                              for j in chunk])
+            grams[t.from_numpy(chunk).to(st.vals.device)] = t.bmm(panels, panels.transpose(1, 2))
+    evals, evecs = t.linalg.eigh(grams[:J])
+    top = evals[:, -1:]
+    keep = (evals > cutoff * top) & (top > 0)
+    inv_vals = t.where(keep, 1.0 / t.where(keep, evals, t.ones_like(evals)), t.zeros_like(evals))
+    inv = t.bmm(evecs * inv_vals[:, None, :], evecs.transpose(1, 2))
+    degenerate = np.nonzero(~D.to_host(keep.all(dim=1)))[0]
+    ranges = [np.arange(j * K, (j + 1) * K) for j in range(J)]
+    return AdditiveSchwarz(system.column_count, ranges, None, tuple(int(j) for j in degenerate),
+                           _device=inv.reshape(-1).contiguous())
+
+
+def cg_normal(operator, rhs: np.ndarray, max_iters: int,
+              monitor: ConvergenceMonitor | None = None,
+              preconditioner: AdditiveSchwarz | None = None) -> SolveResult:
+    """CG on the normal equations from zero (`solvers.py:195-239`), device loop."""
+    blocks, shape = device_operator(operator)
+    rhs = np.asarray(rhs, dtype=float)
+    if rhs.shape != (shape[0],):
+        raise InvalidInputError(f"rhs shape {rhs.shape} != operator rows {shape[0]}")
+    monitor = monitor or ConvergenceMonitor()
+    max_iters = int(max_iters)
+    n, N = int(shape[1]), int(shape[0])
+    t = D.torch()
+    dev = D.require_cuda()
+    f64 = dict(dtype=t.float64, device=dev)
+    nn = max(blocks.ncols_total, 1)
+    buf = {k: t.zeros(nn, **f64) for k in ("p", "q", "r", "x", "xbest")}
+    buf["z"] = t.zeros(nn, **f64) if preconditioner is not None else buf["r"]
+    buf["tmp"] = t.zeros(max(blocks.layout.nrows, 1), **f64)
+    buf["res"] = t.full((max_iters + 2,), float("nan"), **f64)
+    buf["rhs"] = D.to_dev(rhs)
+    buf["scratch"] = t.zeros(2 * 592 + 64, **f64)
+    buf["counter"] = t.zeros(4, dtype=t.int32, device=dev)
+    buf["out"] = t.zeros(1, **f64)
+    stride = max(int(monitor.stride), 1)
+    vecs = _lib.CgVecs(tmp=D.ptr(buf["tmp"]), p=D.ptr(buf["p"]), q=D.ptr(buf["q"]),
+                       r=D.ptr(buf["r"]), z=D.ptr(buf["z"]), x=D.ptr(buf["x"]),
+                       xbest=D.ptr(buf["xbest"]), res_trace=D.ptr(buf["res"]),
+                       rhs=D.ptr(buf["rhs"]), scratch=D.ptr(buf["scratch"]),
+                       counter=D.ptr(buf["counter"]), stride=stride)
+    from .monitor import DeviceL1Error
+    dev_error = isinstance(monitor.error_fn, DeviceL1Error)
+    if dev_error and monitor.error_fn.n != n:
+        raise InvalidInputError(f"error function expects iterates of length {monitor.error_fn.n}, "
+                                f"operator has {n} columns")
+    host_error = monitor.error_fn is not None and not dev_error
+    sst = _lib.LsqrState()
+    sst.best = np.inf
+    sst.best_it = -1
+    sst.stride = stride
+    sst.monitor = 1
+    state = t.from_numpy(np.frombuffer(bytes(sst), dtype=np.uint8).copy()).to(dev)
+    L = _lib.lib()
+    op = C.byref(blocks.struct())
+    pre = C.byref(preconditioner.device_struct()) if preconditioner is not None else None
+    _lib.check(L.fl_cg_init(op, C.byref(vecs), pre, D.ptr(state), D.stream_ptr()), "fl_cg_init")
+    err_trace = None
+    mon = None
+    if dev_error:
+        err_trace = t.full((max_iters + 2,), float("nan"), **f64)
+        mon = monitor.error_fn.struct(err_trace)
+
+    def read():
+        return _lib.LsqrState.from_buffer_copy(D.to_host(state).tobytes())
+
+    if not host_error:
+        _lib.check(L.fl_cg_iterate(op, C.byref(vecs), pre, D.ptr(state), 1, max_iters,
+                                   C.byref(mon) if mon is not None else None, D.stream_ptr()),
+                   "fl_cg_iterate")
+        st = read()
+    else:
+        it = 0
+        st = read()
+        while it < max_iters:
+            count = min(stride - (it % stride), max_iters - it)
+            _lib.check(L.fl_cg_iterate(op, C.byref(vecs), pre, D.ptr(state), it + 1, count, None,
+                                       D.stream_ptr()), "fl_cg_iterate")
+            st = read()
+            done_it = int(st.it)
+            if st.diverged_at:
+                break
+            if done_it % stride == 0 and done_it > it:
+                x_now = D.to_host(buf["x"])[:n]
+                res = float(buf["res"][done_it].item())
+                monitor.observe(done_it, x_now, lambda: res)
+            it += count
+            if st.done:
+                break
+    if st.diverged_at:
+        raise DivergenceError(f"non-finite iterate at iteration {int(st.diverged_at)}")
+    iters = int(st.it)
+    if not host_error:
+        lv = _lib.LsqrVecs(x=D.ptr(buf["x"]), xbest=D.ptr(buf["xbest"]))
+        _lib.check(L.fl_lsqr_monitor_flush(op, C.byref(lv), D.ptr(state), D.stream_ptr()),
+                   "fl_lsqr_monitor_flush")
+    _lib.check(L.fl_cg_residual(op, C.byref(vecs), D.ptr(buf["out"]), D.stream_ptr()),
+               "fl_cg_residual")
+    final_res = float(D.to_host(buf["out"])[0])
+    x = D.to_host(buf["x"])[:n]
+    if not host_error:
+        st = read()
+        res = D.to_host(buf["res"])
+        errs = D.to_host(err_trace) if dev_error else res
+        for it in range(1, iters + 1):
+            if stride > 1 and it % stride != 0:
+                continue
+            monitor.records.append((it, float(res[it]), float(errs[it])))
+        if st.best_it >= 1:
+            monitor.best_error = float(st.best)
+            monitor.best_iteration = int(st.best_it)
+            monitor.best_iterate = D.to_host(buf["xbest"])[:n].copy()
+    return SolveResult(x, iters, final_res, monitor, bool(st.breakdown))

@@ -226,10 +226,38 @@ def masked_golden():
         json.dump(keep, fh, indent=1)
 
 
+def cg_golden():
+    """CG on the normal equations and the additive-Schwarz preconditioner
+    through the reference (solvers.py:150-239): a dense well-conditioned
+    case and cfg1's raw system (plain, and with AS), 200 iterations each."""
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((50, 20))
+    b = rng.standard_normal(50)
+    dense = r_sol.cg_normal(a, b, 40, r_sol.ConvergenceMonitor())
+    wl = workloads.build("cfg1")
+    prob, dec, basis = to_reference(wl)
+    system = r_asm.assemble(prob, dec, basis, interior_per_dim=wl.interior_per_dim)
+    pre = r_sol.as_preconditioner(system)
+    plain = r_sol.cg_normal(system, system.rhs, 200, r_sol.ConvergenceMonitor(stride=5))
+    asc = r_sol.cg_normal(system, system.rhs, 200, r_sol.ConvergenceMonitor(), pre)
+    np.savez_compressed(
+        os.path.join(HERE, "cg.npz"), a=a, b=b, dense_x=dense.solution,
+        dense_records=np.array(dense.monitor.records), dense_res=dense.residual_norm,
+        plain_x=plain.solution, plain_records=np.array(plain.monitor.records),
+        plain_res=plain.residual_norm, plain_best_it=plain.monitor.best_iteration,
+        as_x=asc.solution, as_records=np.array(asc.monitor.records), as_res=asc.residual_norm,
+        as_degenerate=np.array(pre.degenerate_blocks, dtype=np.int64),
+        as_apply=pre.apply(np.linspace(-1, 1, system.column_count)))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["masked"]:
         masked_golden()
         sys.exit(0)
+    if sys.argv[1:] == ["cg"]:
+        cg_golden()
+        sys.exit(0)
+    cg_golden()
     masked_golden()
     demo_report_golden()
     print("reference featlsq", featlsq.__version__, "from", featlsq.__file__)

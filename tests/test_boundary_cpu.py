@@ -52,7 +52,9 @@ def _struct_fields(name):
                                           ("fl_assembly_desc", "AssemblyDesc"),
                                           ("fl_lsqr_state", "LsqrState"),
                                           ("fl_lsqr_vecs", "LsqrVecs"),
-                                          ("fl_test_monitor", "TestMonitor")])
+                                          ("fl_test_monitor", "TestMonitor"),
+                                          ("fl_cg_vecs", "CgVecs"),
+                                          ("fl_block_precond", "BlockPrecond")])
 def test_ctypes_structs_match_header(cname, pyname):
     py = getattr(_lib, pyname)
     assert [f[0] for f in py._fields_] == _struct_fields(cname)

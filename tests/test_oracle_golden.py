@@ -135,3 +135,26 @@ def test_oscillator_demo_seed_reproduces_committed_report(golden_dir):
         assert out["error"] == pytest.approx(s["error"], rel=1e-9)
         assert out["residual"] == pytest.approx(s["residual_norm"], rel=1e-9)
     assert rep["kept"] == 157
+
+
+def test_oracle_cg_and_additive_schwarz_match_reference(golden_dir):
+    """N4: CG on the normal equations (dense case and cfg1's raw system, plain
+    and additive-Schwarz preconditioned) against the reference's own runs."""
+    g = np.load(os.path.join(golden_dir, "cg.npz"))
+    a, b = g["a"], g["b"]
+    x, its, res, recs, brk = O.cg_normal(lambda v: a @ v, lambda r: a.T @ r, 20, b, 40)
+    np.testing.assert_allclose(np.array(recs), g["dense_records"], rtol=1e-12)
+    np.testing.assert_allclose(x, g["dense_x"], rtol=1e-12)
+    wl = workloads.build("cfg1")
+    sysd = O.assemble(wl.problem, wl.dec, wl.basis, wl.interior_per_dim)
+    M = O.raw_operator(sysd)
+    x, its, res, recs, _ = O.cg_normal(lambda v: M @ v, lambda r: M.T @ r, M.shape[1],
+                                       sysd["rhs"], 200, stride=5)
+    np.testing.assert_allclose(np.array(recs)[:, 1], g["plain_records"][:, 1], rtol=1e-6)
+    K = wl.basis.feature_count
+    ranges, invs, deg = O.as_preconditioner([m for _, m in sysd["blocks"]],
+                                            [np.arange(j * K, (j + 1) * K) for j in range(len(sysd["blocks"]))])
+    assert deg == list(g["as_degenerate"])
+    v = np.linspace(-1, 1, M.shape[1])
+    np.testing.assert_allclose(O.as_apply(ranges, invs, v), g["as_apply"], rtol=1e-9,
+                               atol=1e-9 * np.abs(g["as_apply"]).max())
