@@ -159,13 +159,19 @@ def launches_per_step(fs, iters):
 
 def rrqr_flops(m, K, r):
     """F_alg (truncated QRCP + thin Q + initial norms) and
-    F_ref (full dgeqp3 + dorgqr, what the reference executes)."""
+    F_ref (full dgeqp3 + dorgqr, what the reference executes), plus F_exec,
+    what route R executes (DESIGN.md §3 K2): unpivoted QR of A_j, truncated
+    QRCP of R0 (gemv + block updates), Q1 formation, Q0 [Q1; 0]."""
     m, r = m.astype(np.float64), r.astype(np.float64)
     f_alg = (4 * m * K * r - 2 * (m + K) * r ** 2 + (4 / 3) * r ** 3
              + 2 * m * r ** 2 - (2 / 3) * r ** 3 + 2 * m * K)
     kk = np.minimum(m, K)
     f_ref = 4 * m * K * kk - (4 / 3) * kk ** 3
-    return float(f_alg.sum()), float(f_ref.sum())
+    f_exec = ((2 * m * K ** 2 - (2 / 3) * K ** 3)                   # K2a
+              + (4 / 3) * (K ** 3 - (K - r) ** 3)                    # K2b
+              + (2 * K * r ** 2 - (2 / 3) * r ** 3)                  # Q1
+              + 4 * r * (m * K - K ** 2 / 2))                        # K2c
+    return float(f_alg.sum()), float(f_ref.sum()), float(f_exec.sum())
 
 
 # ---------------------------------------------------------------- product arm
@@ -241,7 +247,7 @@ def product(args, rank, world, local_rank):
     m = L.m.astype(np.int64)
     nnz_q = int(np.sum(m * fs.ranks))
     nnz_a = int(m.sum()) * L.K
-    f_alg, f_ref = rrqr_flops(m, L.K, fs.ranks)
+    f_alg, f_ref, f_exec = rrqr_flops(m, L.K, fs.ranks)
     # compulsory bytes of one fused iteration: Q read once (the kernel reuses
     # each staged column tile for Q^T u and Q v'), u/partials, 6 y-space vectors
     bytes_it = 8.0 * (nnz_q + 2 * L.partial_len + 2 * L.nrows + 6 * fs.kept_total)
@@ -283,6 +289,9 @@ def product(args, rank, world, local_rank):
                                     "GFLOP/s_ref": round(f_ref / t_rrqr / 1e9, 1),
                                     "F_alg_TF": round(f_alg / 1e12, 4),
                                     "frac_fp64_peak": round(f_alg / t_rrqr / 1e12 / fp64_peak_tf, 4),
+                                    "F_exec_TF": round(f_exec / 1e12, 4),
+                                    "GFLOP/s_exec": round(f_exec / t_rrqr / 1e9, 1),
+                                    "frac_fp64_peak_exec": round(f_exec / t_rrqr / 1e12 / fp64_peak_tf, 4),
                                     "fp64_peak_TF_measured": fp64},
             "lsqr": {"ms_per_iter": round(t_it * 1e3, 4), "GB/s": round(bytes_it / t_it / 1e9, 1),
                      "frac_hbm": round(bytes_it / t_it / 1e9 / hbm, 4),

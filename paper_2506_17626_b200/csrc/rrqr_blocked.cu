@@ -20,6 +20,9 @@ int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t
                  double* tau, double* T, cudaStream_t s);
 int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
             int32_t* rank, double* diag, cudaStream_t s);
+bool qrcp2_ok(int K);
+int qrcp2_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
+             int32_t* rank, double* diag, cudaStream_t s);
 int wy_apply(const WyArgs& a, cudaStream_t s);
 int wy_nb();
 int wy_tn();
@@ -331,7 +334,15 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
   // ---- K2b: truncated QRCP of R0 ----
   extract_r0_kernel<<<dim3(64, J), 256, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.R0, ws.kmax);
   FL_CHECK_LAUNCH();
-  if ((e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) return e;
+  static const int q2 = [] {
+    const char* e = getenv("FEATLSQ_QRCP2");
+    return e ? atoi(e) : 0;
+  }();
+  if (q2 && fl::qrcp2_ok(K)) {
+    if ((e = fl::qrcp2_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) return e;
+  } else if ((e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) {
+    return e;
+  }
   clamp_tau_kernel<<<J, 256, 0, s>>>(ws.tau1, K, rank);
   build_t_kernel<<<dim3(npan, J), NT, 0, s>>>(ws.R0, K, ws.kmax, ws.tau1, rank, ws.T1);
   init_q1_r_kernel<<<dim3(64, J), 256, 0, s>>>(ws.R0, K, rank, ws.Q1, R);
