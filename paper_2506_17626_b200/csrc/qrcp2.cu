@@ -14,7 +14,8 @@
 // Protocol (mbarriers): full[s] (TMA bytes), empty[s] (the consuming warp),
 // go (consumer thread 0 publishes the step index after the swap; a negative
 // index stops the producer). Column j of step i is global sequence number
-// base_i + j, slot (base_i + j) % NS, consumed by warp j % 16.
+// base_i + j, slot (base_i + j) % NS, issued by producer lane (base_i + j) %
+// 32 and consumed by warp j % 16.
 #include <float.h>
 
 #include "wy.cuh"
@@ -107,27 +108,31 @@ __global__ void __launch_bounds__(NT, 1) qrcp2_kernel(QrcpArgs q) {
   __syncthreads();
 
   // ======================= producer warp =======================
+  // lane l owns ring slot l (NS == 32): it streams the columns whose global
+  // sequence number is l mod 32, so 32 copies are issued in parallel
   if (wid == NCW) {
-    if (lane != 0) return;
-    int64_t g = 0;  // global column sequence number
+    static_assert(NS == 32, "one ring slot per producer lane");
+    int64_t base_p = 0;  // global sequence number of the step's first column
     for (unsigned step = 0;; ++step) {
       mbar_wait(&go, step & 1);
       const int i = *(volatile int*)&s_step;
       if (i < 0) return;
       const int i0 = i & ~1;
       const unsigned bytes = (unsigned)(M - i0) * 8u;
-      for (int c = i + 1; c < N; ++c, ++g) {
-        const int s = (int)(g % NS);
-        if (g >= NS) mbar_wait(&empty[s], (unsigned)(((g / NS) - 1) & 1));
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sa(&full[s])), "r"(bytes)
+      const int ncol = N - i - 1;
+      int64_t g = base_p + ((lane - base_p % NS) + NS) % NS;  // first g >= base_p with g % NS == lane
+      for (; g < base_p + ncol; g += NS) {
+        const int c = i + 1 + (int)(g - base_p);
+        if (g >= NS) mbar_wait(&empty[lane], (unsigned)(((g / NS) - 1) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sa(&full[lane])), "r"(bytes)
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                sa(ring + (int64_t)s * K)),
-            "l"(A + (int64_t)c * K + i0), "r"(bytes), "r"(sa(&full[s]))
+                sa(ring + (int64_t)lane * K)),
+            "l"(A + (int64_t)c * K + i0), "r"(bytes), "r"(sa(&full[lane]))
             : "memory");
       }
+      base_p += ncol;
     }
   }
 
