@@ -136,6 +136,23 @@ def fp64_peak(torch, D, _lib):
     return res
 
 
+def read_peak(torch, D, _lib):
+    """Measured HBM streaming-read ceiling (GB/s), 4 GiB buffer, best of 5."""
+    n = 1 << 29
+    buf = torch.zeros(n, dtype=torch.float64, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    best = 0.0
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(_lib.lib().fl_probe_read(D.ptr(buf), n, D.ptr(out), D.stream_ptr()), "probe")
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 8.0 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del buf
+    return round(best, 1)
+
+
 # ---------------------------------------------------------------- work counts
 def launches_per_step(fs, iters):
     """Kernels of this library launched per solve (rrqr_blocked.cu / qop.cu /
@@ -152,6 +169,13 @@ def launches_per_step(fs, iters):
             k2a = npan + (npan - 1)
             k2c = npan
         rrqr = k2a + 5 + npan + 1 + k2c      # extract, qrcp, clamp, build_t, init_q1_r, Q1, init_qhat
+        # per block group (rrqr_blocked.cu group_count: FEATLSQ_RRQR_GROUPS, default 1,
+        # reduced until every group has >= 32 blocks)
+        g = max(1, min(int(os.environ.get("FEATLSQ_RRQR_GROUPS", "1")), 8))
+        J = fs.qstore.layout.J
+        while g > 1 and J // g < 32:
+            g -= 1
+        rrqr *= g
     else:
         rrqr = 1
     return 1 + rrqr + 2 + 2 * iters + 1      # assemble, rrqr, lsqr init, iterations, recover
@@ -256,6 +280,7 @@ def product(args, rank, world, local_rank):
     t_it = t_lsqr / iters
     hbm, hbm_src = peaks()
     fp64 = fp64_peak(torch, D, _lib)
+    read_gbs = read_peak(torch, D, _lib)
     fp64_peak_tf = max(fp64.values())
     st = state["run"].read_state()
     stage_t = {"assemble": t_asm, "rrqr": t_rrqr, "lsqr": t_lsqr + t_init, "recover": t_rec}
@@ -280,6 +305,9 @@ def product(args, rank, world, local_rank):
                      "achieved": round(bytes_it / t_it / 1e9, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(bytes_it / t_it / 1e9 / hbm, 4),
                      "traffic": traffic, "peak_source": hbm_src,
+                     # the kernel is read-dominated; the copy peak counts read + write
+                     "read_peak_measured": read_gbs,
+                     "frac_of_read_peak": round(bytes_it / t_it / 1e9 / read_gbs, 4),
                      "algorithmic_bytes_per_launch": bytes_it, "dominant_stage": dominant},
         "stages": {
             "assemble": {"ms": round(t_asm * 1e3, 3), "GB/s": round(8 * nnz_a / t_asm / 1e9, 1),

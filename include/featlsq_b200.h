@@ -294,6 +294,8 @@ int fl_backsub_scatter(int32_t nblocks, int32_t K, const double* R, const int32_
 /* diagnostics: FP64 throughput probe (mode 0 DFMA, 1 DMMA m8n8k4); flops
  * per call = grid*256*iters*16 (mode 0) or grid*8*iters*2048 (mode 1) */
 int fl_probe_fp64(int32_t mode, int32_t grid, int32_t iters, double* out, void* stream);
+/* diagnostics: streaming read of n doubles (16-byte loads); bytes = 8 n */
+int fl_probe_read(const double* buf, int64_t n, double* out, void* stream);
 
 /* diagnostics: one batched compact-WY block-reflector launch (DMMA):
  * C_j[row0:m_j, tile] -= V_j op(T_j) V_j^T C_j[row0:m_j, tile] with V_j the

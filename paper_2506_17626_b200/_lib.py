@@ -109,6 +109,7 @@ def lib():
                             C.c_int64, vp],
         "fl_backsub_scatter": [C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp],
         "fl_probe_fp64": [C.c_int32, C.c_int32, C.c_int32, vp, vp],
+        "fl_probe_read": [vp, C.c_int64, vp, vp],
         "fl_rrqr_blocked": [C.POINTER(BlockOp), C.POINTER(BlockOp), C.c_int32, C.c_int64,
                             C.c_double, vp, vp, vp, vp, vp, vp],
         "fl_dev_wy_apply": [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
@@ -144,7 +145,7 @@ EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", 
             "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error",
             "fl_error_blocks", "fl_monitor_error", "fl_lsqr_iterate_monitored",
             "fl_lsqr_monitor_flush", "fl_cg_init", "fl_cg_iterate", "fl_cg_residual",
-            "fl_block_precond_apply")
+            "fl_block_precond_apply", "fl_probe_read")
 
 
 def check(code: int, what: str) -> None:
