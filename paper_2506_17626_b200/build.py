@@ -24,6 +24,8 @@ HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--cudart", "static",
          "-Xptxas", "-v", "-diag-suppress", "177"]
+# tuning experiments only (e.g. FEATLSQ_NVCC_EXTRA="-DWY_STAGES64=4")
+EXTRA = os.environ.get("FEATLSQ_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:
@@ -49,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     log = []
     for src in SOURCES:
         obj = os.path.join(bdir, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc(), *ARCH, *FLAGS, *EXTRA, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         log.append(res.stderr)
         if res.returncode != 0:
