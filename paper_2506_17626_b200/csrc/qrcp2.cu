@@ -22,11 +22,21 @@
 
 namespace {
 
-constexpr int NCW = 16;              // consumer warps
+#ifndef QRCP2_NCW
+#define QRCP2_NCW 16
+#endif
+#ifndef QRCP2_NS
+#define QRCP2_NS 32
+#endif
+constexpr int NCW = QRCP2_NCW;       // consumer warps
 constexpr int NTC = NCW * 32;        // consumer threads
 constexpr int NT = NTC + 32;         // + producer warp
 constexpr int PB = 16;               // panel width (F has PB columns)
-constexpr int NS = 32;               // ring slots (one column segment each)
+constexpr int NS = QRCP2_NS;         // ring slots (one column segment each)
+constexpr int MINB = NCW >= 16 ? 1 : 2;  // CTAs per SM
+// a slot is reused NS columns later by the same consumer warp, so no warp
+// ever waits on a slot's phase two ahead of its last completion
+static_assert(NS % NCW == 0, "ring slots must be a multiple of the consumer warps");
 
 struct QrcpArgs {
   double* R0;
@@ -70,7 +80,7 @@ __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) qrcp2_kernel(QrcpArgs q) {
+__global__ void __launch_bounds__(NT, MINB) qrcp2_kernel(QrcpArgs q) {
   extern __shared__ __align__(128) double sm[];
   const int K = q.K;
   const int j = blockIdx.x;
@@ -108,10 +118,11 @@ __global__ void __launch_bounds__(NT, 1) qrcp2_kernel(QrcpArgs q) {
   __syncthreads();
 
   // ======================= producer warp =======================
-  // lane l owns ring slot l (NS == 32): it streams the columns whose global
-  // sequence number is l mod 32, so 32 copies are issued in parallel
+  // lane l < NS owns ring slot l: it streams the columns whose global
+  // sequence number is l mod NS, so NS copies are issued in parallel
   if (wid == NCW) {
-    static_assert(NS == 32, "one ring slot per producer lane");
+    static_assert(NS <= 32, "one ring slot per producer lane");
+    if (lane >= NS) return;
     int64_t base_p = 0;  // global sequence number of the step's first column
     for (unsigned step = 0;; ++step) {
       mbar_wait(&go, step & 1);
@@ -426,7 +437,7 @@ __global__ void __launch_bounds__(NT, 1) qrcp2_kernel(QrcpArgs q) {
 namespace fl {
 bool qrcp2_ok(int K) {
   const size_t smem = (size_t)((NS + PB + 4) * K) * sizeof(double) + (size_t)2 * K * sizeof(int);
-  return K % 2 == 0 && smem <= 220 * 1024;
+  return K % 2 == 0 && smem <= (MINB > 1 ? 112 : 220) * 1024;
 }
 int qrcp2_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
              int32_t* rank, double* diag, cudaStream_t s) {
