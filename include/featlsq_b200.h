@@ -152,7 +152,9 @@ int fl_rrqr(const fl_blockop* blocks, int32_t K, int32_t max_rows, double sigma,
  * (DMMA trailing updates), truncated QRCP of R0 with LAPACK's dlaqps rule,
  * Q_j = Q0 [Q1; 0]. `A` is left unchanged; Q_j is written to the store `Q`
  * (same layout as A). `workspace` needs fl_rrqr_blocked_workspace() bytes;
- * store_elems = total doubles of the A store. No host synchronisation. */
+ * store_elems = total doubles of the A store. No host synchronisation.
+ * Shared-memory bounds: K <= 640 and max_rows <= 11776 (else FL_ERR_INVALID;
+ * fl_rrqr covers the rest). */
 int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t store_elems);
 int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
                     double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,

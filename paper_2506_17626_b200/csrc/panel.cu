@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
   const int cap = SMEM_S / 8;
   if (8 * M <= cap) panel_body<8>(a, j, S, red, sc, Tw, Vs, Gs);
   else if (4 * M <= cap) panel_body<4>(a, j, S, red, sc, Tw, Vs, Gs);
-  else panel_body<2>(a, j, S, red, sc, Tw, Vs, Gs);
+  else if (2 * M <= cap) panel_body<2>(a, j, S, red, sc, Tw, Vs, Gs);
+  else __trap();  // excluded by rrqr_route (filtering.py BLOCKED_MAX_ROWS) and panel_factor
 }
 
 }  // namespace

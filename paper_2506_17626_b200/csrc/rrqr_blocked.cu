@@ -424,6 +424,8 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
   if (!(sigma >= 0.0 && sigma < 1.0) || K < NB || K % NB) return FL_ERR_INVALID;
   const int J = A->nblocks;
   if (J == 0) return FL_OK;
+  // shared-memory bounds of K2a (>= 2 staged panel columns) and K2b (F panel)
+  if (A->max_rows > 11776 || K > 640) return FL_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   Workspace ws = carve(workspace, J, K, store_elems, nullptr);
   // the raw blocks stay intact: factor a copy (same layout, absolute offsets)

@@ -119,3 +119,17 @@ def test_product_path_refuses_without_gpu():
     wl = workloads.build("cfg1")
     with pytest.raises(fl.DeviceError):
         fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+
+
+def test_rrqr_route_respects_shared_memory_bounds():
+    from paper_2506_17626_b200._device import BlockLayout
+    from paper_2506_17626_b200.filtering import BLOCKED_MAX_K, BLOCKED_MAX_ROWS, rrqr_route
+
+    def layout(K, m):
+        return BlockLayout(m, K, [np.arange(m), np.arange(m)])
+    assert rrqr_route(layout(512, 2700)) == "blocked"
+    assert rrqr_route(layout(64, 300)) == "direct"                 # K < 128
+    assert rrqr_route(layout(200, 900)) == "direct"                # K % 32 != 0
+    assert rrqr_route(layout(512, 400)) == "direct"                # wide blocks
+    assert rrqr_route(layout(BLOCKED_MAX_K + 32, 2000)) == "direct"
+    assert rrqr_route(layout(256, BLOCKED_MAX_ROWS + 16)) == "direct"

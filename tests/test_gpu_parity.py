@@ -254,6 +254,23 @@ def test_qr_edge_cases(fl):
     assert fl.qr_column_pivot(dup, 1e-8).kept.size == 5
 
 
+@pytest.mark.parametrize("K", [256, 704])
+def test_qr_column_pivot_both_routes_match_scipy(fl, K):
+    """K = 256 takes route R (blocked), K = 704 exceeds its shared-memory
+    bound and takes the direct kernel: both reproduce LAPACK's kept sequence
+    on a gapped-spectrum matrix (linalg.py:58-97)."""
+    rng = np.random.default_rng(K)
+    m = 900
+    u, _ = np.linalg.qr(rng.standard_normal((m, K)))
+    w, _ = np.linalg.qr(rng.standard_normal((K, K)))
+    s = np.logspace(0, -14, K)
+    a = (u * s) @ w.T
+    _, r_ref, kept_ref, _, _ = O.qr_column_pivot(a, 1e-10)
+    got = fl.qr_column_pivot(a, 1e-10)
+    assert np.array_equal(got.kept, kept_ref)
+    assert np.linalg.norm(got.r_factor - r_ref) <= 1e-10 * np.linalg.norm(r_ref)
+
+
 # ---------------------------------------------------------------- LSQR unit cases
 @pytest.fixture(scope="module")
 def tall(golden_dir):
