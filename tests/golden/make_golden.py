@@ -250,7 +250,30 @@ def cg_golden():
         as_apply=pre.apply(np.linspace(-1, 1, system.column_count)))
 
 
+def activations_golden():
+    """sin and sigmoid feature networks (basis.py:24-40) through the reference
+    assembly: 1D soft-constrained oscillator and 2D masked laplace."""
+    cases = {
+        "osc_sin": (r_prob.oscillator_problem(60.0), 20, 2.9, 8, "sin"),
+        "osc_sigmoid": (r_prob.oscillator_problem(60.0), 20, 2.9, 8, "sigmoid"),
+        "lap_sigmoid": (r_prob.laplace_problem(3), 4, 2.9, 16, "sigmoid"),
+        "lap_sin": (r_prob.laplace_problem(3), 4, 2.9, 16, "sin"),
+    }
+    out = {}
+    for name, (prob, S, ov, K, act) in cases.items():
+        dec = r_dom.decompose(prob.domain, S, ov)
+        basis = r_basis.init_basis(dec, K, 1, act, r_lin.RandomSource(0).generator())
+        system = r_asm.assemble(prob, dec, basis)
+        out[name + "_rhs"] = system.rhs
+        out[name + "_rows"] = np.concatenate([b.rows for b in system.blocks])
+        out[name + "_vals"] = np.concatenate([b.matrix.ravel() for b in system.blocks])
+    np.savez_compressed(os.path.join(HERE, "activations.npz"), **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["activations"]:
+        activations_golden()
+        sys.exit(0)
     if sys.argv[1:] == ["masked"]:
         masked_golden()
         sys.exit(0)
@@ -258,6 +281,7 @@ if __name__ == "__main__":
         cg_golden()
         sys.exit(0)
     cg_golden()
+    activations_golden()
     masked_golden()
     demo_report_golden()
     print("reference featlsq", featlsq.__version__, "from", featlsq.__file__)

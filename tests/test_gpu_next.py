@@ -169,3 +169,17 @@ def test_laplace_demo_through_device_path(fl, golden_dir):
     pred = fl.evaluate_solution(p, dec, basis, coeffs, ts.points)
     err = fl.l1_error(pred, ts)
     assert err == pytest.approx(mon.best_error, rel=1e-6)
+
+
+@pytest.mark.parametrize("name", ["lap_sigmoid", "lap_sin", "osc_sigmoid", "osc_sin"])
+def test_activations_assembly_matches_reference(fl, name, golden_dir):
+    """K1 with sin / sigmoid features (basis.py:24-40) against the reference."""
+    from test_oracle_masked import activation_case
+    g = np.load(os.path.join(golden_dir, "activations.npz"))
+    p, dec, basis = activation_case(name)
+    sysd = fl.assemble(p, dec, basis)
+    assert np.array_equal(np.concatenate([b.rows for b in sysd.blocks]), g[name + "_rows"])
+    np.testing.assert_allclose(sysd.rhs, g[name + "_rhs"], rtol=1e-13,
+                               atol=1e-14 * np.abs(g[name + "_rhs"]).max())
+    vals = np.concatenate([b.matrix.ravel() for b in sysd.blocks])
+    assert np.abs(vals - g[name + "_vals"]).max() <= 1e-13 * np.abs(g[name + "_vals"]).max()

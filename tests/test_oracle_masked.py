@@ -79,3 +79,32 @@ def test_laplace_demo_reproduces_committed_report(golden_dir):
     assert out["drop_fraction"] == s["drop_fraction"]
     assert out["error"] == pytest.approx(s["error"], rel=1e-12)
     assert out["residual"] == pytest.approx(s["residual_norm"], rel=1e-12)
+
+
+ACT_CASES = {"osc_sin": ("osc", "sin"), "osc_sigmoid": ("osc", "sigmoid"),
+             "lap_sigmoid": ("lap", "sigmoid"), "lap_sin": ("lap", "sin")}
+
+
+def activation_case(name):
+    from paper_2506_17626_b200.problems import oscillator_problem
+    kind, act = ACT_CASES[name]
+    if kind == "osc":
+        p, S, K = oscillator_problem(60.0), 20, 8
+    else:
+        p, S, K = laplace_problem(3), 4, 16
+    dec = decompose(p.domain, S, 2.9)
+    return p, dec, init_basis(dec, K, 1, act, O.random_source(0))
+
+
+@pytest.mark.parametrize("name", sorted(ACT_CASES))
+def test_oracle_activations_match_reference(name, golden_dir):
+    """sin / sigmoid feature jets (basis.py:24-40) through the oracle's
+    assembly against the reference's."""
+    g = np.load(os.path.join(golden_dir, "activations.npz"))
+    p, dec, basis = activation_case(name)
+    sysd = O.assemble(p, dec, basis, None)
+    assert np.array_equal(np.concatenate([r for r, _ in sysd["blocks"]]), g[name + "_rows"])
+    np.testing.assert_allclose(sysd["rhs"], g[name + "_rhs"], rtol=1e-13,
+                               atol=1e-14 * np.abs(g[name + "_rhs"]).max())
+    vals = np.concatenate([m.ravel() for _, m in sysd["blocks"]])
+    assert np.abs(vals - g[name + "_vals"]).max() <= 1e-13 * np.abs(g[name + "_vals"]).max()
