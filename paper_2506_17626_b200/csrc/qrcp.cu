@@ -26,7 +26,16 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
-constexpr int PB = 16;  // panel width (F has PB columns)
+#ifndef QRCP_PB
+#define QRCP_PB 16
+#endif
+#ifndef QRCP_CU
+#define QRCP_CU 8
+#endif
+#ifndef QRCP_MB
+#define QRCP_MB 2
+#endif
+constexpr int PB = QRCP_PB;  // panel width (F has PB columns)
 
 struct QrcpArgs {
   double* R0;          // (J, K, K) column-major, ld K; on exit: R above, reflectors below
@@ -51,7 +60,7 @@ __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 2) qrcp_kernel(QrcpArgs q) {
+__global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   extern __shared__ double sm[];
   const int K = q.K;
   const int j = blockIdx.x;
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(NT, 2) qrcp_kernel(QrcpArgs q) {
         const int ncol = N - i - 1;
         // 16-byte loads: lane owns rows (2l, 2l+1) of each 64-row chunk, starting at
         // the even row i0 <= i (row i-1 contributes v = 0); two chunks per trip
-        constexpr int CU = 8;  // columns in flight per warp
+        constexpr int CU = QRCP_CU;  // columns in flight per warp
         const int i0 = i & ~1;
         for (int c0 = wid * CU; c0 < ncol; c0 += NW * CU) {
           double d[CU];
