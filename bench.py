@@ -286,10 +286,12 @@ def product(args, rank, world, local_rank):
     stage_t = {"assemble": t_asm, "rrqr": t_rrqr, "lsqr": t_lsqr + t_init, "recover": t_rec}
     dominant = max(stage_t, key=stage_t.get)
     step_s = elapsed / args.steps
-    traffic = None
+    traffic = asm_flops = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(args.config, {}).get("lsqr_bytes_per_iter")
+        tj = json.load(open(tpath)).get(args.config, {})
+        traffic = tj.get("lsqr_bytes_per_iter")
+        asm_flops = tj.get("assemble_fp64_flops")
     out = {
         "metric": METRIC, "value": round(whole_job_rate(world, 1, step_s), 6), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -311,7 +313,11 @@ def product(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": bytes_it, "dominant_stage": dominant},
         "stages": {
             "assemble": {"ms": round(t_asm * 1e3, 3), "GB/s": round(8 * nnz_a / t_asm / 1e9, 1),
-                         "frac_hbm": round(8 * nnz_a / t_asm / 1e9 / hbm, 4)},
+                         "frac_hbm": round(8 * nnz_a / t_asm / 1e9 / hbm, 4),
+                         **({"TF/s_fp64": round(asm_flops / t_asm / 1e12, 2),
+                             "frac_fp64_dfma_peak": round(asm_flops / t_asm / 1e12 / fp64["dfma"], 4),
+                             "fp64_flops_source": "ncu SASS counts, profiles/traffic.json"}
+                            if asm_flops else {})},
             "rrqr_filter_precond": {"ms": round(t_rrqr * 1e3, 3),
                                     "GFLOP/s_alg": round(f_alg / t_rrqr / 1e9, 1),
                                     "GFLOP/s_ref": round(f_ref / t_rrqr / 1e9, 1),
