@@ -438,3 +438,25 @@ def test_oscillator_demo_matches_committed_report(fl, golden_dir):
         assert res.iterations_run == s["iterations_run"]
         assert res.residual_norm == pytest.approx(s["residual_norm"], rel=1e-6)
         assert 0.4 * s["error"] <= err <= 2.5 * s["error"]
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_fallback_paths_agree(fl, name, monkeypatch):
+    """The two-pass LSQR kernels (used when a column does not fit on chip)
+    and the direct RRQR kernel (used outside route R's bounds) give the same
+    results as the default fused / blocked paths on the same input."""
+    wl, ref, fb, off, sysd, fs = runs(fl, name)
+    op = fl.precondition(fs)
+    fused = fl.lsqr(op, sysd.rhs, 60)
+    monkeypatch.setenv("FEATLSQ_LSQR", "split")
+    split = fl.lsqr(op, sysd.rhs, 60)
+    monkeypatch.delenv("FEATLSQ_LSQR")
+    np.testing.assert_allclose([r[1] for r in split.monitor.records],
+                               [r[1] for r in fused.monitor.records], rtol=1e-10)
+    assert np.linalg.norm(split.solution - fused.solution) <= 1e-8 * np.linalg.norm(fused.solution)
+    monkeypatch.setenv("FEATLSQ_RRQR", "direct")
+    fd = fl.filter_system(sysd, wl.sigma)
+    monkeypatch.delenv("FEATLSQ_RRQR")
+    assert np.array_equal(fd.kept_columns, fs.kept_columns)
+    for a, b in zip(fd.blocks, fs.blocks):
+        assert np.linalg.norm(a.r_factor - b.r_factor) <= 1e-10 * np.linalg.norm(b.r_factor)
