@@ -8,7 +8,8 @@
 //   p_j    += Q_j[:, tile] v'_j[tile]                       (second use of the same tile)
 //
 // A column tile (W columns, all m_j rows) is staged once in shared memory
-// (TMA bulk copies into an ST-deep mbarrier ring) and used by both products,
+// (one TMA bulk copy per column into a ring of SL single-column slots, each
+// with its own mbarrier) and used by both products,
 // because p_j = Q_j v'_j = sum over tiles of Q_j[:, tile] v'_j[tile] needs
 // each tile's own entries only. The normalisation v_{k+1} = v'/alpha_{k+1}
 // (alpha is a grid-wide norm) is applied afterwards by linearity in the row
@@ -25,9 +26,11 @@
 // split over S CTAs (S <= FL_LSQR_SPLIT_MAX), each writing its own copy of
 // p_j, which the row kernel sums in a fixed order — finer work units shorten
 // the tail of the last wave. The CTA shape (NT threads, RP row pairs per thread,
-// W columns per tile, ST ring stages) is picked per layout from the
-// instantiated table at the bottom: NT = 256 runs two CTAs per SM so one
-// block's prologue/epilogue overlaps another block's stream.
+// W columns per barrier, SL ring slots, MB CTAs per SM) is picked per layout
+// from the instantiated table at the bottom: at cfg4 (ld <= 3072) 256 threads
+// and two CTAs per SM, so one block's prologue/epilogue overlaps another
+// block's stream. Each thread reads its row pairs as 16-byte shared loads and
+// keeps them in registers between the two products.
 #include <float.h>
 #include <math.h>
 #include <stdio.h>
