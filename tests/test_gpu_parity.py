@@ -460,3 +460,23 @@ def test_fallback_paths_agree(fl, name, monkeypatch):
     assert np.array_equal(fd.kept_columns, fs.kept_columns)
     for a, b in zip(fd.blocks, fs.blocks):
         assert np.linalg.norm(a.r_factor - b.r_factor) <= 1e-10 * np.linalg.norm(b.r_factor)
+
+
+def test_blocked_route_sigma_zero_keeps_all(fl):
+    """Route R with sigma = 0 keeps min(m, K) = K columns of every block
+    (linalg.py:75-85), in LAPACK's pivot order down to the rounding floor:
+    once |R_ii| / |R_00| is ~1e-16 the remaining pivots are decided by
+    rounding noise in any implementation, so the order is compared while
+    the reference's ratio is above 1e-12."""
+    from paper_2506_17626_b200.filtering import rrqr_route
+    wl, ref, fb, off, sysd, fs = runs(fl, "cfg2")
+    assert rrqr_route(sysd.store.layout) == "blocked"
+    full = fl.filter_system(sysd, 0.0)
+    K = wl.basis.feature_count
+    assert np.all(full.ranks == K)
+    for j in (0, len(full.kept_list) // 2):
+        got = full.kept_list[j] - j * K
+        assert np.array_equal(np.sort(got), np.arange(K))
+        _, _, kept_ref, _, ratios = O.qr_column_pivot(ref["blocks"][j][1], 0.0)
+        n = int(np.sum(ratios > 1e-12))
+        assert n >= 5 and np.array_equal(got[:n], kept_ref[:n])
