@@ -57,3 +57,32 @@ def test_full_size_kept_sequences_match_reference(fl, name, golden_dir):
     np.testing.assert_allclose(fro, g["r_fro"], rtol=1e-10)
     del fs, sysd
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["cfg4"])
+def test_full_size_lsqr_properties(fl, name):
+    """LSQR at the BASELINE size, through size-independent properties: the
+    residual estimate phibar is non-increasing and equals the true residual
+    ||Q y - b|| (to 1e-9 relative after 60 iterations, SURVEY §0 F3 keeps it
+    from being exact), the device run is bit-reproducible, and the recovered
+    coefficients reproduce Q y through the raw blocks (M a = Q y)."""
+    import torch
+    from paper_2506_17626_b200 import workloads
+    wl = workloads.build(name)
+    sysd = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    fs = fl.filter_system(sysd, wl.sigma)
+    op = fl.precondition(fs)
+    r1 = fl.lsqr(op, sysd.rhs, 60)
+    r2 = fl.lsqr(op, sysd.rhs, 60)
+    assert np.array_equal(r1.solution, r2.solution)
+    ph = np.array([r[1] for r in r1.monitor.records])
+    assert np.all(np.diff(ph) <= 1e-12 * ph[0])
+    qy = op.apply(r1.solution)
+    true_res = np.linalg.norm(qy - sysd.rhs)
+    assert r1.residual_norm == pytest.approx(true_res, rel=1e-9)
+    a = fl.recover_solution(fs, r1.solution)
+    ma = fl.apply(sysd, a)
+    # M a = Q y up to eps * kappa(R_j) (kappa ~ 1e10 at sigma = 1e-10)
+    assert np.linalg.norm(ma - qy) <= 1e-4 * np.linalg.norm(qy)
+    del fs, sysd, op
+    torch.cuda.empty_cache()
