@@ -148,7 +148,13 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         if (r < i) {
           if (p != i) ci[r] = xp;
         } else {
-          for (int kk = 0; kk < k; ++kk) xp -= A[(int64_t)(offset + kk) * K + r] * F[kk * K + p];
+          // the panel values are loaded together (one round trip, not k)
+          double pa[PB];
+#pragma unroll
+          for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk < k) ? A[(int64_t)(offset + kk) * K + r] : 0.0;
+#pragma unroll
+          for (int kk = 0; kk < PB; ++kk)
+            if (kk < k) xp -= pa[kk] * F[kk * K + p];
           v[r - i] = xp;
         }
       }
@@ -256,7 +262,14 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         for (int kk = wid; kk < k; kk += NW) {
           const double* cc = A + (int64_t)(offset + kk) * K;
           double dd = 0.0;
-          for (int r = i + lane; r < M; r += 32) dd += cc[r] * v[r - i];
+          for (int r0 = i + lane; r0 < M; r0 += 32 * 8) {  // 8 loads in flight per lane
+            double x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[q] = (r0 + 32 * q < M) ? cc[r0 + 32 * q] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (r0 + 32 * q < M) dd += x[q] * v[r0 + 32 * q - i];
+          }
           dd = fl::warp_sum(dd);
           if (lane == 0) auxv[kk] = -t * dd;
         }
