@@ -15,9 +15,10 @@
 //
 // The step's critical path is a handful of dependent memory round trips, so
 // the kernel is organised for memory-level parallelism: the column swap is
-// fused with the pivot column's panel update, the F-gemv keeps four columns
-// in flight per warp, and row i of the trailing columns is prefetched while
-// the F-gemv runs.
+// fused with the pivot column's panel update (whose k panel values per row
+// are loaded together), the F-gemv keeps eight columns x two 64-row chunks
+// in flight per warp with 16-byte loads, and the auxv dots issue eight loads
+// per lane at a time.
 #include <float.h>
 
 #include "wy.cuh"
