@@ -20,15 +20,33 @@ constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~38 
 constexpr int GC = 64;              // Gram pass row chunk
 constexpr int GLD = GC + 4;
 
-// Sum `n` (<= 32) per-thread partials across the CTA; results in out[0..n).
-__device__ __forceinline__ void block_sums(const double* part, int n, double* red, double* out) {
+// Sum N (a power of two <= 32) per-thread partials across the CTA; results
+// in out[0..N). Within a warp a butterfly halves the live values per lane at
+// each of the first log2(N) steps (N - 1 shuffles instead of 5 N), then the
+// remaining steps sum the single value; lane (32 / N) c ends with value c.
+template <int N>
+__device__ __forceinline__ void block_sums(const double (&part)[N], double* red, double* out) {
+  static_assert(N >= 1 && N <= 32 && (N & (N - 1)) == 0, "power of two <= 32");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = 0; i < n; ++i) {
-    double v = fl::warp_sum(part[i]);
-    if (lane == 0) red[wid * 32 + i] = v;
+  double v[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) v[c] = part[c];
+#pragma unroll
+  for (int half = N / 2, o = 16; half >= 1; half /= 2, o /= 2) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int c = 0; c < half; ++c) {
+      const double send = up ? v[c] : v[c + half];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+      v[c] = (up ? v[c + half] : v[c]) + recv;
+    }
   }
+  double sv = v[0];
+#pragma unroll
+  for (int o = 32 / N / 2; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+  if ((lane & (32 / N - 1)) == 0) red[wid * 32 + lane / (32 / N)] = sv;
   __syncthreads();
-  if (threadIdx.x < n) {
+  if (threadIdx.x < N) {
     double s = 0.0;
     for (int w = 0; w < NW; ++w) s += red[w * 32 + threadIdx.x];
     out[threadIdx.x] = s;
@@ -55,7 +73,7 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
     double part[1] = {0.0};
     for (int r = i + 1 + threadIdx.x; r < Mq; r += NT) part[0] += si[r] * si[r];
     const double alpha = si[i];
-    block_sums(part, 1, red, sc);
+    block_sums<1>(part, red, sc);
     const double xnorm = sqrt(sc[0]);
     double beta, t;
     if (xnorm == 0.0) {
@@ -88,7 +106,7 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
         }
       }
     }
-    block_sums(p, 2 * W, red, sc);
+    block_sums<2 * W>(p, red, sc);
     // T column i (dlarft forward, columnwise): T[0:i, i] = -t * T[0:i,0:i] * (V_prev^T v_i)
     if (threadIdx.x < i) {
       const int a = threadIdx.x;
@@ -119,9 +137,15 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
   for (int q = 0; q < NB / W; ++q) {
     const int c = P0 + q * W;
     const int Mq = m - c;
-    // load inner panel rows c..m-1
+    // load inner panel rows c..m-1 (8-byte cp.async: every load in flight at once)
     for (int k = 0; k < W; ++k)
-      for (int r = threadIdx.x; r < Mq; r += NT) S[k * Mq + r] = Aj[(int64_t)(c + k) * ld + c + r];
+#pragma unroll 2
+      for (int r = threadIdx.x; r < Mq; r += NT) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(S + k * Mq + r);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(Aj + (int64_t)(c + k) * ld + c + r)
+                     : "memory");
+      }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     factor_inner<W>(S, Mq, red, sc, Tw, tau_j, c);
     for (int k = 0; k < W; ++k)
@@ -131,6 +155,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
       double p[4 * W];
 #pragma unroll
       for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
+#pragma unroll 2
       for (int r = threadIdx.x; r < Mq; r += NT) {
         double xv[4];
 #pragma unroll
@@ -142,7 +167,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
           for (int u = 0; u < 4; ++u) p[k * 4 + u] += v * xv[u];
         }
       }
-      block_sums(p, 4 * W, red, sc);
+      block_sums<4 * W>(p, red, sc);
       // z = Tw^T w  (W x 4)
       __shared__ double z[4 * 8];
       if (threadIdx.x < 4 * W) {
@@ -152,6 +177,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
         z[k * 4 + u] = s;
       }
       __syncthreads();
+#pragma unroll 2
       for (int r = threadIdx.x; r < Mq; r += NT) {
         double vv[W];
 #pragma unroll
@@ -185,16 +211,31 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
       }
   }
   double acc0 = 0.0, acc1 = 0.0;
-  for (int r0 = 0; r0 < M; r0 += GC) {
-    for (int p = threadIdx.x; p < NB * GC; p += NT) {
-      const int col = p / GC, rr = p % GC, row = r0 + rr;
+  // the next chunk's V values are loaded into registers while this one is
+  // multiplied (one round trip per chunk overlapped instead of exposed)
+  constexpr int PER = NB * GC / NT;
+  static_assert(PER * NT == NB * GC, "chunk must split evenly over the CTA");
+  double nx[PER];
+  auto fetch = [&](int r0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int p = threadIdx.x + q * NT, col = p / GC, rr = p % GC, row = r0 + rr;
       double v = 0.0;
       if (row < M) {
         if (row > col) v = Aj[(int64_t)(P0 + col) * ld + P0 + row];
         else if (row == col) v = 1.0;
       }
-      Vs[col * GLD + rr] = v;
+      nx[q] = v;
     }
+  };
+  fetch(0);
+  for (int r0 = 0; r0 < M; r0 += GC) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int p = threadIdx.x + q * NT;
+      Vs[(p / GC) * GLD + p % GC] = nx[q];
+    }
+    if (r0 + GC < M) fetch(r0 + GC);
     __syncthreads();
     if (w < 10) {
 #pragma unroll 4
