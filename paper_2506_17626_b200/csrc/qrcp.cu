@@ -160,6 +160,20 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         }
       }
       __syncthreads();
+      // row i of the trailing columns (final once the swap is done) and of
+      // the panel columns: 8-byte cp.async into shared memory, waited for
+      // only before the row update, so the round trip overlaps dlarfg and the
+      // gemv without holding registers
+      for (int c = i + 1 + threadIdx.x; c < N; c += NT)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(rowA + c)),
+                     "l"(A + (int64_t)c * K + i)
+                     : "memory");
+      if (threadIdx.x < k)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(rowi + threadIdx.x)),
+                     "l"(A + (int64_t)(offset + threadIdx.x) * K + i)
+                     : "memory");
       if (p != i) {
         if (threadIdx.x < k) {
           const double t = F[threadIdx.x * K + i];
@@ -202,6 +216,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           s_stop = 1;
           s_rank = i;
         }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");  // no copies in flight at exit
         __syncthreads();
         break;
       }
@@ -213,8 +228,6 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           ci[r] = x;  // reflector below the diagonal
         }
       }
-      // prefetch row i of the trailing columns for the row update
-      for (int c = i + 1 + threadIdx.x; c < N; c += NT) rowA[c] = A[(int64_t)c * K + i];
       __syncthreads();
       if (threadIdx.x == 0) {
         v[0] = 1.0;
@@ -274,8 +287,8 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           dd = fl::warp_sum(dd);
           if (lane == 0) auxv[kk] = -t * dd;
         }
-        if (threadIdx.x <= k)
-          rowi[threadIdx.x] = (threadIdx.x == k) ? 1.0 : A[(int64_t)(offset + threadIdx.x) * K + i];
+        if (threadIdx.x == k) rowi[k] = 1.0;
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
       }
       __syncthreads();
       // ---- F(:, k) += F(:, 0:k) auxv (F(offset..i, k) = 0 first);
