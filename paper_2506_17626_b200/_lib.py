@@ -14,7 +14,7 @@ from .errors import (DegenerateSubdomainError, DeviceError, DivergenceError,
                      InvalidInputError, SingularFactorError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfeatlsq_b200.so")
+LIB_PATH = os.environ.get("FEATLSQ_LIB") or os.path.join(HERE, "libfeatlsq_b200.so")
 
 FL_OK, FL_ERR_INVALID, FL_ERR_DEGENERATE, FL_ERR_DIVERGENCE, FL_ERR_SINGULAR, FL_ERR_CUDA = \
     0, -1, -2, -3, -4, -5

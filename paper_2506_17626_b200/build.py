@@ -17,7 +17,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libfeatlsq_b200.so")
+# FEATLSQ_LIB: alternative output path for tuning builds (default in-tree)
+LIB = os.environ.get("FEATLSQ_LIB") or os.path.join(HERE, "libfeatlsq_b200.so")
 SOURCES = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(ROOT, "include", "featlsq_b200.h")]
@@ -46,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     objs = []
-    bdir = os.path.join(HERE, "_build")
+    bdir = os.path.join(HERE, "_build", os.path.basename(LIB))
     os.makedirs(bdir, exist_ok=True)
     log = []
     for src in SOURCES:

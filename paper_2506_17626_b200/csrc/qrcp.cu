@@ -20,6 +20,7 @@
 // in flight per warp with 16-byte loads, and the auxv dots issue eight loads
 // per lane at a time.
 #include <float.h>
+#include <stdlib.h>
 
 #include "wy.cuh"
 
@@ -32,6 +33,12 @@ constexpr int NW = NT / 32;
 #endif
 #ifndef QRCP_CU
 #define QRCP_CU 8
+#endif
+#ifndef QRCP_NTL
+#define QRCP_NTL 2
+#endif
+#ifndef QRCP_EARLY_CLOSE
+#define QRCP_EARLY_CLOSE 0  // 1: dlaqps's literal early panel close on a flagged norm
 #endif
 #ifndef QRCP_MB
 #define QRCP_MB 2
@@ -47,6 +54,7 @@ struct QrcpArgs {
   int32_t* perm;       // (J, K)
   int32_t* rank;       // (J,)
   double* diag;        // (J, K) |R_ii| / |R_00|
+  int J;
 };
 
 __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
@@ -64,7 +72,7 @@ __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
 __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   extern __shared__ double sm[];
   const int K = q.K;
-  const int j = blockIdx.x;
+  for (int j = blockIdx.x; j < q.J; j += gridDim.x) {
   const int M = q.kmax[j];
   const int N = K;
   double* F = sm;                    // [PB][K]  F[k*K + c]
@@ -306,8 +314,12 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             tt = fmax(0.0, (1.0 + tt) * (1.0 - tt));
             const double rr = vn1[c] / vn2[c];
             if (tt * rr * rr <= tol3z) {
+#if QRCP_EARLY_CLOSE
               flag[c] = 1;
               s_flagged = 1;
+#else
+              flag[atomicAdd(&s_flagged, 1)] = c;
+#endif
             } else {
               vn1[c] *= sqrt(tt);
             }
@@ -315,6 +327,35 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         }
       }
       __syncthreads();
+#if !QRCP_EARLY_CLOSE
+      // ---- flagged columns: instead of closing the panel (dlaqps), their
+      //      norms are recomputed now from the panel-updated values
+      //      A(i+1:M, c) - A(i+1:M, offset:i+1) F(c, 0:k+1)^T, which are what
+      //      the block update would leave there (same exact-arithmetic value,
+      //      no extra pass over the trailing matrix) ----
+      if (s_flagged) {
+        const int nf = s_flagged;
+        for (int f = wid; f < nf; f += NW) {
+          const int c = flag[f];
+          double s2 = 0.0;
+          for (int r = i + 1 + lane; r < M; r += 32) {
+            double pa[PB];
+#pragma unroll
+            for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk <= k) ? A[(int64_t)(offset + kk) * K + r] : 0.0;
+            double x = A[(int64_t)c * K + r];
+#pragma unroll
+            for (int kk = 0; kk < PB; ++kk)
+              if (kk <= k) x -= pa[kk] * F[kk * K + c];
+            s2 += x * x;
+          }
+          s2 = fl::warp_sum(s2);
+          if (lane == 0) vn1[c] = vn2[c] = (i + 1 < M) ? sqrt(s2) : 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_flagged = 0;
+        __syncthreads();
+      }
+#endif
       ++k;
     }
     if (s_stop) break;
@@ -322,46 +363,73 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
     const int rk = offset + kb;
     // ---- block update: A(rk:M, rk:N) -= A(rk:M, offset:rk) F(rk:N, 0:kb)^T  (DMMA) ----
     if (rk < M && rk < N) {
-      // warp = 8-row strip; the strip's panel fragments stay in registers and the
-      // 8-column tiles are software pipelined (next tile loaded before this one
-      // is stored) so the loop is not one memory round trip per tile
+      // The MMA's m index is the trailing column and its n index the row, so
+      // a lane's accumulator pair is two adjacent rows of one column (one
+      // 16-byte load / store) and a warp instruction covers 8 columns x 64 B.
+      // A warp owns an 8*NTL-row strip (NTL n-tiles; the panel values of its rows
+      // stay in registers as B fragments, zero outside rk..M-1 so those rows
+      // are rewritten unchanged) and walks 8-column tiles with the next tile's
+      // accumulators loaded before the current one is computed.
+      constexpr int KS = PB / 4, NTL = QRCP_NTL;
       const int g = lane >> 2, t4 = lane & 3;
-      const int nrt = (M - rk + 7) / 8, nct = (N - rk + 7) / 8;
-      for (int rt = wid; rt < nrt; rt += NW) {
-        const int row = rk + rt * 8 + g;
-        const bool rok = row < M;
-        double av[PB / 4];
+      const int r0 = rk & ~7;
+      const int nrs = (M - r0 + 8 * NTL - 1) / (8 * NTL);
+      const int ncg = nrs >= NW ? 1 : NW / nrs;
+      const int nct = (N - rk + 7) / 8;
+      for (int item = wid; item < nrs * ncg; item += NW) {
+        const int rs = r0 + (item % nrs) * 8 * NTL;
+        double bq[NTL][KS];
 #pragma unroll
-        for (int s = 0; s < PB / 4; ++s) {
-          const int kk = 4 * s + t4;
-          av[s] = (rok && kk < kb) ? -A[(int64_t)(offset + kk) * K + row] : 0.0;
-        }
-        auto ld = [&](int ct, double& x0, double& x1) {
-          const int c0 = rk + ct * 8 + 2 * t4;
-          x0 = (rok && c0 < N) ? A[(int64_t)c0 * K + row] : 0.0;
-          x1 = (rok && c0 + 1 < N) ? A[(int64_t)(c0 + 1) * K + row] : 0.0;
-        };
-        double d0, d1;
-        ld(0, d0, d1);
-        for (int ct = 0; ct < nct; ++ct) {
-          double n0 = 0.0, n1 = 0.0;
-          if (ct + 1 < nct) ld(ct + 1, n0, n1);
-          const int cb = rk + ct * 8 + g;
+        for (int t = 0; t < NTL; ++t) {
+          const int row = rs + 8 * t + g;
 #pragma unroll
-          for (int s = 0; s < PB / 4; ++s) {
-            const int kk = 4 * s + t4;
-            const double bv = (cb < N && kk < kb) ? F[kk * K + cb] : 0.0;
-            fl::dmma(d0, d1, av[s], bv);
+          for (int s2 = 0; s2 < KS; ++s2) {
+            const int kk = 4 * s2 + t4;
+            bq[t][s2] = (row >= rk && row < M && kk < kb) ? A[(int64_t)(offset + kk) * K + row] : 0.0;
           }
-          const int c0 = rk + ct * 8 + 2 * t4;
-          if (rok && c0 < N) A[(int64_t)c0 * K + row] = d0;
-          if (rok && c0 + 1 < N) A[(int64_t)(c0 + 1) * K + row] = d1;
-          d0 = n0;
-          d1 = n1;
+        }
+        auto ldc = [&](int ct, double2* c) {
+          const int col = rk + ct * 8 + g;
+#pragma unroll
+          for (int t = 0; t < NTL; ++t) {
+            const int row = rs + 8 * t + 2 * t4;
+            c[t] = (col < N && row < M) ? *reinterpret_cast<const double2*>(A + (int64_t)col * K + row)
+                                        : make_double2(0.0, 0.0);
+          }
+        };
+        double2 cc[NTL], cn[NTL], cn2[NTL];
+        int ct = item / nrs;
+        if (ct < nct) ldc(ct, cc);
+        if (ct + ncg < nct) ldc(ct + ncg, cn);
+        for (; ct < nct; ct += ncg) {
+          if (ct + 2 * ncg < nct) ldc(ct + 2 * ncg, cn2);
+          const int col = rk + ct * 8 + g;
+          double af[KS];
+#pragma unroll
+          for (int s2 = 0; s2 < KS; ++s2) {
+            const int kk = 4 * s2 + t4;
+            af[s2] = (col < N && kk < kb) ? -F[kk * K + col] : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < NTL; ++t)
+#pragma unroll
+            for (int s2 = 0; s2 < KS; ++s2) fl::dmma(cc[t].x, cc[t].y, af[s2], bq[t][s2]);
+          // accumulator lane layout: c[g][2 t4 + e] = A(rs + 8t + 2 t4 + e, rk + 8ct + g)
+#pragma unroll
+          for (int t = 0; t < NTL; ++t) {
+            const int row = rs + 8 * t + 2 * t4;
+            if (col < N && row < M) *reinterpret_cast<double2*>(A + (int64_t)col * K + row) = cc[t];
+          }
+#pragma unroll
+          for (int t = 0; t < NTL; ++t) {
+            cc[t] = cn[t];
+            cn[t] = cn2[t];
+          }
         }
       }
     }
     __syncthreads();
+#if QRCP_EARLY_CLOSE
     // ---- recompute flagged norms over rows rk..M-1 ----
     for (int c = rk + wid; c < N; c += NW) {
       if (!flag[c]) continue;
@@ -374,6 +442,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
     }
     __syncthreads();
+#endif
     offset = rk;
   }
   __syncthreads();
@@ -384,6 +453,8 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         (c < rank && lead > 0.0) ? q.diag[(int64_t)j * K + c] / lead : 0.0;
   }
   if (threadIdx.x == 0) q.rank[j] = rank;
+  __syncthreads();
+  }
 }
 
 }  // namespace
@@ -394,8 +465,10 @@ int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double*
   const size_t smem = (size_t)(PB * K + 4 * K) * sizeof(double) + (size_t)2 * K * sizeof(int);
   if (smem > 110 * 1024) return FL_ERR_INVALID;
   FL_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  QrcpArgs a{R0, K, kmax, sigma, tau, perm, rank, diag};
-  qrcp_kernel<<<J, NT, smem, s>>>(a);
+  QrcpArgs a{R0, K, kmax, sigma, tau, perm, rank, diag, J};
+  int grid = J;
+  if (const char* e = getenv("FEATLSQ_QRCP_GRID")) grid = max(1, min(J, atoi(e)));
+  qrcp_kernel<<<grid, NT, smem, s>>>(a);
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
