@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   __shared__ double redv[NW];
   __shared__ int redi[NW];
   __shared__ double auxv[PB];
+  __shared__ double fred[8 * NW];
   __shared__ double rowi[PB + 1];
   __shared__ int s_stop, s_rank, s_flagged, s_p;
 
@@ -334,24 +335,50 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       //      the block update would leave there (same exact-arithmetic value,
       //      no extra pass over the trailing matrix) ----
       if (s_flagged) {
+        // all threads share the rows; the panel values of a row are loaded
+        // once for up to FB flagged columns, warp partials summed in order
+        constexpr int FB = 4;
         const int nf = s_flagged;
-        for (int f = wid; f < nf; f += NW) {
-          const int c = flag[f];
-          double s2 = 0.0;
-          for (int r = i + 1 + lane; r < M; r += 32) {
+        for (int f0 = 0; f0 < nf; f0 += FB) {
+          const int nb = min(FB, nf - f0);
+          double s2[FB];
+#pragma unroll
+          for (int f = 0; f < FB; ++f) s2[f] = 0.0;
+          for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
             double pa[PB];
 #pragma unroll
             for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk <= k) ? A[(int64_t)(offset + kk) * K + r] : 0.0;
-            double x = A[(int64_t)c * K + r];
+            double x[FB];
 #pragma unroll
-            for (int kk = 0; kk < PB; ++kk)
-              if (kk <= k) x -= pa[kk] * F[kk * K + c];
-            s2 += x * x;
+            for (int f = 0; f < FB; ++f) x[f] = (f < nb) ? A[(int64_t)flag[f0 + f] * K + r] : 0.0;
+#pragma unroll
+            for (int f = 0; f < FB; ++f) {
+              if (f < nb) {
+                const int c = flag[f0 + f];
+#pragma unroll
+                for (int kk = 0; kk < PB; ++kk)
+                  if (kk <= k) x[f] -= pa[kk] * F[kk * K + c];
+                s2[f] += x[f] * x[f];
+              }
+            }
           }
-          s2 = fl::warp_sum(s2);
-          if (lane == 0) vn1[c] = vn2[c] = (i + 1 < M) ? sqrt(s2) : 0.0;
+#pragma unroll
+          for (int f = 0; f < FB; ++f) {
+            if (f < nb) {
+              const double w = fl::warp_sum(s2[f]);
+              if (lane == 0) fred[f * NW + wid] = w;
+            }
+          }
+          __syncthreads();
+          if (threadIdx.x < nb) {
+            double t2 = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t2 += fred[threadIdx.x * NW + w];
+            const int c = flag[f0 + threadIdx.x];
+            vn1[c] = vn2[c] = (i + 1 < M) ? sqrt(t2) : 0.0;
+          }
+          __syncthreads();
         }
-        __syncthreads();
         if (threadIdx.x == 0) s_flagged = 0;
         __syncthreads();
       }
