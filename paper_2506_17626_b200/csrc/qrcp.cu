@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   double* F = sm;                    // [PB][K]  F[k*K + c]
   double* vn1 = F + PB * K;
   double* vn2 = vn1 + K;
-  double* v = vn2 + K;               // reflector rows i..M-1 (v[0] = 1)
+  double* v = vn2 + K;               // pivot column rows i..M-1 (unscaled)
   double* rowA = v + K;              // prefetched A(i, c) of the trailing columns
   int* piv = (int*)(rowA + K);
   int* flag = piv + K;
@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   __syncthreads();
 
   double lead = 0.0;
+  int s_pl = 0;
   int offset = 0;
   while (offset < M && !s_stop) {
     const int nbp = min(PB, M - offset);
@@ -138,19 +139,18 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           redi[wid] = bi;
         }
         __syncthreads();
-        if (wid == 0) {
-          bv = lane < NW ? redv[lane] : -1.0;
-          bi = lane < NW ? redi[lane] : N;
-          argmax_lowest(bv, bi);
-          if (lane == 0) s_p = bi;
-        }
-        __syncthreads();
+        // every warp reduces the NW candidates itself (no second barrier)
+        bv = lane < NW ? redv[lane] : -1.0;
+        bi = lane < NW ? redi[lane] : N;
+        argmax_lowest(bv, bi);
+        s_pl = bi;
       }
-      const int p = s_p;
+      const int p = s_pl;
       // ---- swap columns i <-> p fused with the pivot column's panel update:
       //      v = A(i:M, p) - A(i:M, offset:i) F(p, 0:k)^T ----
       double* ci = A + (int64_t)i * K;
       double* cp = A + (int64_t)p * K;
+      double ss = 0.0;  // dlarfg's ||v(i+1:M)||^2, summed as the column is formed
       for (int r = threadIdx.x; r < M; r += NT) {
         const double xi = ci[r];
         double xp = cp[r];
@@ -166,8 +166,11 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           for (int kk = 0; kk < PB; ++kk)
             if (kk < k) xp -= pa[kk] * F[kk * K + p];
           v[r - i] = xp;
+          if (r > i) ss += xp * xp;
         }
       }
+      ss = fl::warp_sum(ss);
+      if (lane == 0) red[wid] = ss;
       __syncthreads();
       // row i of the trailing columns (final once the swap is done) and of
       // the panel columns: 8-byte cp.async into shared memory, waited for
@@ -200,12 +203,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           flag[i] = f;
         }
       }
-      // ---- dlarfg ----
-      double ss = 0.0;
-      for (int r = i + 1 + threadIdx.x; r < M; r += NT) ss += v[r - i] * v[r - i];
-      ss = fl::warp_sum(ss);
-      if (lane == 0) red[wid] = ss;
-      __syncthreads();
+      // ---- dlarfg (the norm's warp partials are in red) ----
       ss = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) ss += red[w];
@@ -229,22 +227,17 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         __syncthreads();
         break;
       }
-      {
-        const double scal = (xnorm == 0.0) ? 1.0 : 1.0 / (alpha - beta);
-        for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
-          const double x = v[r - i] * scal;
-          v[r - i] = x;
-          ci[r] = x;  // reflector below the diagonal
-        }
-      }
-      __syncthreads();
+      // v stays unscaled in shared memory: its readers below form
+      // w_r = v[r-i] * scal (the value dlarfg's dscal stores, bit for bit)
+      // and w_i = 1 themselves, which saves two barriers per step
+      const double scal = (xnorm == 0.0) ? 1.0 : 1.0 / (alpha - beta);
+      for (int r = i + 1 + threadIdx.x; r < M; r += NT) ci[r] = v[r - i] * scal;  // reflector below the diagonal
       if (threadIdx.x == 0) {
-        v[0] = 1.0;
         tau[i] = t;
         ci[i] = beta;
         q.diag[(int64_t)j * K + i] = fabs(beta);
       }
-      __syncthreads();
+      auto wv = [&](int r) { return r == i ? 1.0 : v[r - i] * scal; };
       // ---- F(i+1:N, k) = t A(i:M, i+1:N)^T v ; auxv = -t A(i:M, offset:i)^T v ----
       {
         const int ncol = N - i - 1;
@@ -262,11 +255,11 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           }
           for (int r = i0 + 2 * lane; r < M; r += 128) {
             const int r2 = r + 64;
-            const double v0 = (r >= i) ? v[r - i] : 0.0;
-            const double v1 = (r + 1 < M) ? v[r + 1 - i] : 0.0;
+            const double v0 = (r >= i) ? wv(r) : 0.0;
+            const double v1 = (r + 1 < M) ? wv(r + 1) : 0.0;
             const bool two = r2 < M;
-            const double w0 = two ? v[r2 - i] : 0.0;
-            const double w1 = (r2 + 1 < M) ? v[r2 + 1 - i] : 0.0;
+            const double w0 = two ? wv(r2) : 0.0;
+            const double w1 = (r2 + 1 < M) ? wv(r2 + 1) : 0.0;
             double2 x[CU], y[CU];
 #pragma unroll
             for (int u = 0; u < CU; ++u) {
@@ -291,7 +284,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             for (int q = 0; q < 8; ++q) x[q] = (r0 + 32 * q < M) ? cc[r0 + 32 * q] : 0.0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (r0 + 32 * q < M) dd += x[q] * v[r0 + 32 * q - i];
+              if (r0 + 32 * q < M) dd += x[q] * wv(r0 + 32 * q);
           }
           dd = fl::warp_sum(dd);
           if (lane == 0) auxv[kk] = -t * dd;
