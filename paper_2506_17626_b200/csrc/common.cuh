@@ -36,6 +36,32 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Warp sums of N (a power of two <= 32) per-lane values with N - 1 + log2(32/N)
+// shuffles instead of 5 N: the first log2(N) butterfly levels halve the live
+// values per lane; afterwards every lane l holds the full sum of value
+// l / (32 / N). Fixed order, so results are run-to-run reproducible.
+template <int N>
+__device__ __forceinline__ double warp_multi_sum(const double (&in)[N]) {
+  const int lane = threadIdx.x & 31;
+  double v[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) v[c] = in[c];
+#pragma unroll
+  for (int half = N / 2, o = 16; half >= 1; half /= 2, o /= 2) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int c = 0; c < half; ++c) {
+      const double send = up ? v[c] : v[c + half];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+      v[c] = (up ? v[c + half] : v[c]) + recv;
+    }
+  }
+  double s = v[0];
+#pragma unroll
+  for (int o = 32 / N / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 // Deterministic CTA-wide sum (fixed shuffle tree, fixed warp order). Every
 // thread gets the result. `sh` needs blockDim.x/32 doubles.
 __device__ __forceinline__ double block_sum(double v, double* sh) {

@@ -269,10 +269,10 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
 #pragma unroll
             for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
           }
-#pragma unroll
-          for (int u = 0; u < CU; ++u) {
-            const double s = fl::warp_sum(d[u]);
-            if (lane == 0 && c0 + u < ncol) F[k * K + i + 1 + c0 + u] = t * s;
+          {
+            const double s = fl::warp_multi_sum<CU>(d);  // lane l: column u = l / (32 / CU)
+            const int u = lane / (32 / CU);
+            if ((lane & (32 / CU - 1)) == 0 && c0 + u < ncol) F[k * K + i + 1 + c0 + u] = t * s;
           }
         }
         for (int kk = wid; kk < k; kk += NW) {
