@@ -1,0 +1,276 @@
+// K2c, fused form: Q_j = Q0_j [Q1_j; 0] with ONE pass over Q per 64-reflector
+// block of Q0_j instead of two.
+//
+// Q0_j = H_0 .. H_{K-1} is applied to C = [Q1_j; 0] block by block in reverse
+// (b = nb-1 .. 0), each block in compact-WY form C -= V_b T_b (V_b^T C). The
+// two-pass kernel (wy.cu) streams C once for W_b = V_b^T C and once for the
+// update. Here one CTA owns a 64-column tile of C for the whole sequence, so
+// the update pass of block b also accumulates W_{b-1} = V_{b-1}^T C from the
+// freshly updated rows (rows >= 64(b-1); rows 64(b-1)..64b-1 are read by the
+// same pass since V_b vanishes there). The sequence is
+//     B(nb-1) ; A(nb-1)+B(nb-2) ; ... ; A(1)+B(0) ; A(0)
+// (A = apply, B = accumulate), nb + 1 passes over C instead of 2 nb, and the
+// first one only reads rows 64(nb-1)..K-1 because C is zero below row K
+// until A(nb-1) runs (which also skips loading those rows).
+//
+// Every product is mma.sync m8n8k4 f64 (DMMA), as in wy.cu. Chunks of 32
+// rows of [V_{b-1} | V_b] (128 columns) and C (64 columns) are staged with
+// 16-byte cp.async in a 3-stage ring. Between passes the ring's memory holds
+// W and T_{b-1} for W' = T_{b-1} W, whose fragments are then kept in
+// registers for the next pass's update.
+#include "wy.cuh"
+
+namespace {
+
+constexpr int NB = 64;    // reflectors per block
+constexpr int TN = 64;    // C columns per CTA
+constexpr int RC = 32;    // rows per staged chunk
+constexpr int LDS = RC + 4;
+constexpr int LDW = TN + 4;
+constexpr int NW = 16, NT = NW * 32;
+#ifndef QF_STAGES
+#define QF_STAGES 3
+#endif
+constexpr int STAGES = QF_STAGES;
+constexpr int VST = 2 * NB * LDS;  // doubles per V stage: V_{b-1} columns 0..63, V_b columns 64..127
+constexpr int CST = TN * LDS;
+constexpr size_t SMEM = (size_t)STAGES * (VST + CST) * sizeof(double);
+static_assert((size_t)(NB * LDW + NB * NB) * sizeof(double) <= SMEM, "W and T fit in the ring");
+
+struct QfArgs {
+  const double* V;       // factored A store (reflectors below the diagonal)
+  const int64_t* voff;
+  const int32_t* vld;
+  const int32_t* m;
+  double* C;             // Q store, holding [Q1; 0] on entry
+  const int64_t* coff;
+  const int32_t* cld;
+  const int32_t* rank;   // columns of C per block
+  const double* T64;     // (J, K/64, 64, 64) column-major upper-triangular T_b
+  int K;
+  int tiles_per_block;
+};
+
+__global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
+  extern __shared__ double sm[];
+  double* Vs = sm;                      // [STAGES][128][LDS]
+  double* Cs = Vs + STAGES * VST;       // [STAGES][64][LDS]
+  double* Ws = sm;                      // between passes: [64][LDW]
+  double* Ts = sm + NB * LDW;           //                 [64][64]
+
+  const int j = blockIdx.x / a.tiles_per_block;
+  const int c0 = (blockIdx.x % a.tiles_per_block) * TN;
+  const int mj = a.m[j];
+  const int ncol = min(TN, a.rank[j] - c0);
+  if (ncol <= 0 || mj <= 0) return;
+  const int K = a.K;
+  const int vld = a.vld[j], cld = a.cld[j];
+  const double* V = a.V + a.voff[j];
+  double* C = a.C + a.coff[j] + (int64_t)c0 * cld;
+  const double* Tj = a.T64 + (int64_t)j * (K / NB) * NB * NB;
+  const int nact = min(K / NB, (mj + NB - 1) / NB);  // blocks with reflectors
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+
+  // this thread's two (column, row pair) staging slots of a 64 x RC tile
+  int scol[2], srr[2];
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int p = threadIdx.x + it * NT;
+    scol[it] = p / (RC / 2);
+    srr[it] = (p % (RC / 2)) * 2;
+  }
+
+  // phase-B warp tiles (W = V^T C, 64 x 64, rows split over two k groups)
+  const int kg = w / (NW / 2), wl = w % (NW / 2);
+  const int mb = wl % 4, nbk = wl / 4;
+  // phase-A warp tiles (C -= V W', 32 x 64): two m-tiles x one n-tile
+  const int mp = w % 2, nt = w / 2;
+
+  double bw[NB / 4];  // W'(4k + t, 8 nt + g)
+  double acc[2][4][2];
+
+  int bA = -1, bB = nact - 1;
+  for (;;) {
+    const bool doA = bA >= 0, doB = bB >= 0;
+    const int rlo = doB ? NB * bB : NB * bA;
+    const int rhi = doA ? mj : min(mj, K);
+    // C rows >= K are zero until the first update has run
+    const int cz = (bA == nact - 1 || !doA) ? K : cld;
+    const int nch = (rhi - rlo + RC - 1) / RC;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
+
+    auto load = [&](int ch) {
+      const int rbase = rlo + ch * RC, s = ch % STAGES;
+      double* vs = Vs + s * VST;
+      double* cs = Cs + s * CST;
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int col = scol[it], rr = srr[it], row = rbase + rr;
+        if (doB) {
+          double* d = vs + col * LDS + rr;
+          if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bB + col) * vld + row);
+          else d[0] = d[1] = 0.0;
+        }
+        if (doA) {
+          double* d = vs + (NB + col) * LDS + rr;
+          if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bA + col) * vld + row);
+          else d[0] = d[1] = 0.0;
+        }
+        double* d = cs + col * LDS + rr;
+        if (col < ncol && row < cz && row < cld) fl::cp_async16(d, C + (int64_t)col * cld + row);
+        else d[0] = d[1] = 0.0;
+      }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nch) load(s);
+      fl::cp_async_commit();
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+      const int rbase = rlo + ch * RC;
+      if (ch + STAGES - 1 < nch) load(ch + STAGES - 1);
+      fl::cp_async_commit();
+      fl::cp_async_wait<STAGES - 1>();
+      __syncthreads();
+      double* vs = Vs + (ch % STAGES) * VST;
+      double* cs = Cs + (ch % STAGES) * CST;
+      // unit lower-trapezoidal structure: V_b's diagonal starts at row 64 b
+      const bool mB = doB && rbase < NB * bB + NB, mA = doA && rbase < NB * bA + NB;
+      if (mB || mA) {
+        for (int p = threadIdx.x; p < NB * RC; p += NT) {
+          const int col = p / RC, rr = p % RC;
+          if (mB) {
+            const int rel = rbase + rr - NB * bB;
+            if (rel <= col) vs[col * LDS + rr] = (rel == col) ? 1.0 : 0.0;
+          }
+          if (mA) {
+            const int rel = rbase + rr - NB * bA;
+            if (rel <= col) vs[(NB + col) * LDS + rr] = (rel == col) ? 1.0 : 0.0;
+          }
+        }
+        __syncthreads();
+      }
+      // ---- A: C -= V_b W' on this chunk (rows above 64 b are untouched) ----
+      if (doA && rbase + RC > NB * bA) {
+        const double* vb = vs + NB * LDS;
+        double c[2][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int row = (2 * mp + mi) * 8 + g, col = nt * 8 + 2 * t;
+          c[mi][0] = cs[col * LDS + row];
+          c[mi][1] = cs[(col + 1) * LDS + row];
+        }
+#pragma unroll
+        for (int k = 0; k < NB / 4; ++k) {
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+            fl::dmma(c[mi][0], c[mi][1], -vb[(4 * k + t) * LDS + (2 * mp + mi) * 8 + g], bw[k]);
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int row = (2 * mp + mi) * 8 + g, col = nt * 8 + 2 * t;
+          cs[col * LDS + row] = c[mi][0];
+          cs[(col + 1) * LDS + row] = c[mi][1];
+          if (rbase + row < mj) {
+            if (col < ncol) C[(int64_t)col * cld + rbase + row] = c[mi][0];
+            if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + rbase + row] = c[mi][1];
+          }
+        }
+        if (doB) __syncthreads();
+      }
+      // ---- B: W_{b-1} += V_{b-1}^T C on the (updated) chunk ----
+      if (doB) {
+#pragma unroll
+        for (int s = kg; s < RC / 4; s += 2) {
+          const int k0 = 4 * s;
+          double av[2], bv[4];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((2 * mb + mi) * 8 + g) * LDS + k0 + t];
+#pragma unroll
+          for (int n = 0; n < 4; ++n) bv[n] = cs[((4 * nbk + n) * 8 + g) * LDS + k0 + t];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) fl::dmma(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
+        }
+      }
+      __syncthreads();  // the stage is refilled by a later iteration
+    }
+    if (!doB) break;
+
+    // ---- between passes: W' = T_{b-1} W in the ring's memory, fragments to registers ----
+    fl::cp_async_wait<0>();
+    __syncthreads();
+    if (kg == 1) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const int row = (2 * mb + mi) * 8 + g, col = (4 * nbk + n) * 8 + 2 * t;
+          Ws[row * LDW + col] = acc[mi][n][0];
+          Ws[row * LDW + col + 1] = acc[mi][n][1];
+        }
+    }
+    for (int i = threadIdx.x; i < NB * NB; i += NT) Ts[i] = Tj[(int64_t)bB * NB * NB + i];
+    __syncthreads();
+    if (kg == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const int row = (2 * mb + mi) * 8 + g, col = (4 * nbk + n) * 8 + 2 * t;
+          Ws[row * LDW + col] += acc[mi][n][0];
+          Ws[row * LDW + col + 1] += acc[mi][n][1];
+        }
+    }
+    __syncthreads();
+    {
+      const int mt = w % (NB / 8), ntb = (w / (NB / 8)) * 4;
+      double p2[4][2];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) p2[n][0] = p2[n][1] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double av = Ts[(k0 + t) * NB + mt * 8 + g];  // T[mt*8+g][k0+t]
+#pragma unroll
+        for (int n = 0; n < 4; ++n) fl::dmma(p2[n][0], p2[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = p2[n][0];
+        Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = p2[n][1];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < NB / 4; ++k) bw[k] = Ws[(4 * k + t) * LDW + nt * 8 + g];
+    __syncthreads();  // the ring is reloaded by the next pass
+    bA = bB;
+    --bB;
+  }
+}
+
+}  // namespace
+
+namespace fl {
+// Q (blocks at coff/cld, holding [Q1; 0]) <- Q0 Q for every block; K % 64 == 0.
+int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
+                const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int K, int J,
+                cudaStream_t s) {
+  if (K % NB) return FL_ERR_INVALID;
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA(cudaFuncSetAttribute(qform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr = true;
+  }
+  QfArgs a{V, voff, vld, m, C, coff, cld, rank, T64, K, (K + TN - 1) / TN};
+  qform_kernel<<<J * a.tiles_per_block, NT, SMEM, s>>>(a);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+}  // namespace fl

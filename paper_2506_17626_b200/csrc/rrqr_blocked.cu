@@ -26,6 +26,9 @@ int qrcp2_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double
 int wy_apply(const WyArgs& a, cudaStream_t s);
 int wy_nb();
 int wy_tn();
+int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
+                const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int K, int J,
+                cudaStream_t s);
 }  // namespace fl
 
 namespace {
@@ -373,6 +376,11 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
   // ---- K2c: Qhat = Q0 [Q1; 0], reflector blocks of Q0 in reverse ----
   init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, (double*)Q->vals);
   FL_CHECK_LAUNCH();
+  static const int qf = [] {
+    const char* e = getenv("FEATLSQ_QFORM");  // 0: two-pass wy_apply per reflector block
+    return e ? atoi(e) : 1;
+  }();
+  if (wide && qf) return fl::qform_fused(fac, A->off, A->ld, A->m, (double*)Q->vals, Q->off, Q->ld, rank, ws.T64, K, J, s);
   const int wb = wide ? 64 : NB;
   for (int p = K / wb - 1; p >= 0; --p) {
     const int P0 = p * wb;
