@@ -41,6 +41,34 @@ __global__ void __launch_bounds__(256) dmma_probe(int iters, double* out) {
   if (s == 12345.678) out[0] = s;
 }
 
+// DMMA with CH independent accumulator chains per warp; LDSOP: the A operand
+// of every DMMA is a fresh shared-memory load (the pattern of the WY kernels)
+template <int CH, bool LDSOP>
+__global__ void __launch_bounds__(512) dmma_chain_probe(int iters, double* out) {
+  __shared__ double sa[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) sa[i] = 1e-3 * i;
+  __syncthreads();
+  double c[CH][2];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) c[k][0] = c[k][1] = 0.0;
+  const double a0 = 1e-3 * (threadIdx.x & 7), b = 1e-3 * (threadIdx.x >> 3);
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const double a = LDSOP ? sa[((i * CH + k) * 36 + lane) & 1023] : a0;
+      asm volatile(
+          "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c[k][0]), "+d"(c[k][1])
+          : "d"(a), "d"(b));
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) s += c[k][0] + c[k][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 // streaming read of n doubles with 16-byte loads, four in flight per thread
 __global__ void __launch_bounds__(256) read_probe(const double2* __restrict__ a, int64_t n2, double* out) {
   double s = 0.0;
@@ -69,10 +97,20 @@ extern "C" int fl_probe_read(const double* buf, int64_t n, double* out, void* st
 // flops per call: mode 0: grid*256*iters*8*2; mode 1: grid*8 warps*iters*4*512
 extern "C" int fl_probe_fp64(int32_t mode, int32_t grid, int32_t iters, double* out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (mode == 0)
-    dfma_probe<<<grid, 256, 0, s>>>(iters, out);
-  else
-    dmma_probe<<<grid, 256, 0, s>>>(iters, out);
+  switch (mode) {
+    case 0: dfma_probe<<<grid, 256, 0, s>>>(iters, out); break;
+    case 1: dmma_probe<<<grid, 256, 0, s>>>(iters, out); break;
+    // diagnostic: 512-thread CTAs, flops = grid*16 warps*iters*CH*512
+    case 11: dmma_chain_probe<1, false><<<grid, 512, 0, s>>>(iters, out); break;
+    case 12: dmma_chain_probe<2, false><<<grid, 512, 0, s>>>(iters, out); break;
+    case 14: dmma_chain_probe<4, false><<<grid, 512, 0, s>>>(iters, out); break;
+    case 18: dmma_chain_probe<8, false><<<grid, 512, 0, s>>>(iters, out); break;
+    case 21: dmma_chain_probe<1, true><<<grid, 512, 0, s>>>(iters, out); break;
+    case 22: dmma_chain_probe<2, true><<<grid, 512, 0, s>>>(iters, out); break;
+    case 24: dmma_chain_probe<4, true><<<grid, 512, 0, s>>>(iters, out); break;
+    case 28: dmma_chain_probe<8, true><<<grid, 512, 0, s>>>(iters, out); break;
+    default: return FL_ERR_INVALID;
+  }
   FL_CHECK_LAUNCH();
   return FL_OK;
 }

@@ -16,8 +16,10 @@
 // Every product is mma.sync m8n8k4 f64 (DMMA), as in wy.cu. Chunks of 32
 // rows of [V_{b-1} | V_b] (128 columns) and C (64 columns) are staged with
 // 16-byte cp.async in a 3-stage ring. Between passes the ring's memory holds
-// W and T_{b-1} for W' = T_{b-1} W, whose fragments are then kept in
-// registers for the next pass's update.
+// W and T_{b-1} for W' = T_{b-1} W, which is kept in shared memory behind
+// the ring for the next pass's update. (Measured alternative, not kept:
+// warps split into an update group and an accumulate group one chunk apart,
+// one barrier per chunk: 69% DMMA pipe activity but 94.6 vs 91.3 ms.)
 #include "wy.cuh"
 
 namespace {
@@ -34,8 +36,11 @@ constexpr int NW = 16, NT = NW * 32;
 constexpr int STAGES = QF_STAGES;
 constexpr int VST = 2 * NB * LDS;  // doubles per V stage: V_{b-1} columns 0..63, V_b columns 64..127
 constexpr int CST = TN * LDS;
-constexpr size_t SMEM = (size_t)STAGES * (VST + CST) * sizeof(double);
-static_assert((size_t)(NB * LDW + NB * NB) * sizeof(double) <= SMEM, "W and T fit in the ring");
+constexpr size_t RING = (size_t)STAGES * (VST + CST) * sizeof(double);
+// W' = T W stays in shared memory behind the ring (as registers it pins 32 of
+// the 128 per thread and the compiler then serialises the A-fragment loads)
+constexpr size_t SMEM = RING + (size_t)NB * LDW * sizeof(double);
+static_assert((size_t)(NB * LDW + NB * NB) * sizeof(double) <= RING, "W and T fit in the ring");
 
 struct QfArgs {
   const double* V;       // factored A store (reflectors below the diagonal)
@@ -57,6 +62,7 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
   double* Cs = Vs + STAGES * VST;       // [STAGES][64][LDS]
   double* Ws = sm;                      // between passes: [64][LDW]
   double* Ts = sm + NB * LDW;           //                 [64][64]
+  double* Wp = sm + RING / sizeof(double);  // W' [64][LDW], persistent
 
   const int j = blockIdx.x / a.tiles_per_block;
   const int c0 = (blockIdx.x % a.tiles_per_block) * TN;
@@ -86,7 +92,6 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
   // phase-A warp tiles (C -= V W', 32 x 64): two m-tiles x one n-tile
   const int mp = w % 2, nt = w / 2;
 
-  double bw[NB / 4];  // W'(4k + t, 8 nt + g)
   double acc[2][4][2];
 
   int bA = -1, bB = nact - 1;
@@ -166,9 +171,10 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
         }
 #pragma unroll
         for (int k = 0; k < NB / 4; ++k) {
+          const double b = Wp[(4 * k + t) * LDW + nt * 8 + g];  // W'(4k + t, 8 nt + g)
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
-            fl::dmma(c[mi][0], c[mi][1], -vb[(4 * k + t) * LDS + (2 * mp + mi) * 8 + g], bw[k]);
+            fl::dmma(c[mi][0], c[mi][1], -vb[(4 * k + t) * LDS + (2 * mp + mi) * 8 + g], b);
         }
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi) {
@@ -242,14 +248,11 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
       __syncthreads();
 #pragma unroll
       for (int n = 0; n < 4; ++n) {
-        Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = p2[n][0];
-        Ws[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = p2[n][1];
+        Wp[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = p2[n][0];
+        Wp[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = p2[n][1];
       }
-      __syncthreads();
     }
-#pragma unroll
-    for (int k = 0; k < NB / 4; ++k) bw[k] = Ws[(4 * k + t) * LDW + nt * 8 + g];
-    __syncthreads();  // the ring is reloaded by the next pass
+    __syncthreads();  // W' complete; the ring is reloaded by the next pass
     bA = bB;
     --bB;
   }
