@@ -16,7 +16,8 @@ namespace {
 constexpr int NB = 32;
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
-constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~38 KB static <= 227 KB)
+constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
+// (measured: 256 threads at two CTAs per SM, 84 KB panels, was slower: 2.80 vs 2.25 ms per launch)
 constexpr int GC = 64;              // Gram pass row chunk
 constexpr int GLD = GC + 4;
 
@@ -197,20 +198,26 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
   __syncthreads();  // every inner panel written back; S is reused as the staging buffer
   const int M = m - P0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
-  // upper-triangular 8x8 tiles (ta <= tb): 10 tiles, warps 0..9
-  int ta = 0, tb = 0;
-  {
-    int idx = w, cnt = 0;
+  // upper-triangular 8x8 tiles (ta <= tb): 10 tiles, tile w and (with fewer
+  // than 10 warps) tile w + NW per warp
+  constexpr int NTW = (10 + NW - 1) / NW;
+  int ta[NTW], tb[NTW];
+#pragma unroll
+  for (int q = 0; q < NTW; ++q) {
+    ta[q] = tb[q] = -1;
+    int idx = w + q * NW, cnt = 0;
     for (int x = 0; x < 4; ++x)
       for (int y = x; y < 4; ++y) {
         if (cnt == idx) {
-          ta = x;
-          tb = y;
+          ta[q] = x;
+          tb[q] = y;
         }
         ++cnt;
       }
   }
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc[NTW][2];
+#pragma unroll
+  for (int q = 0; q < NTW; ++q) acc[q][0] = acc[q][1] = 0.0;
   // the next chunk's V values are loaded into registers while this one is
   // multiplied (one round trip per chunk overlapped instead of exposed)
   constexpr int PER = NB * GC / NT;
@@ -237,22 +244,28 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
     }
     if (r0 + GC < M) fetch(r0 + GC);
     __syncthreads();
-    if (w < 10) {
+#pragma unroll
+    for (int q = 0; q < NTW; ++q) {
+      if (ta[q] >= 0) {
 #pragma unroll 4
-      for (int k0 = 0; k0 < GC; k0 += 4)
-        fl::dmma(acc0, acc1, Vs[(ta * 8 + g) * GLD + k0 + t4], Vs[(tb * 8 + g) * GLD + k0 + t4]);
+        for (int k0 = 0; k0 < GC; k0 += 4)
+          fl::dmma(acc[q][0], acc[q][1], Vs[(ta[q] * 8 + g) * GLD + k0 + t4], Vs[(tb[q] * 8 + g) * GLD + k0 + t4]);
+      }
     }
     __syncthreads();
   }
-  if (w < 10) {
-    Gs[(ta * 8 + g) * NB + tb * 8 + 2 * t4] = acc0;
-    Gs[(ta * 8 + g) * NB + tb * 8 + 2 * t4 + 1] = acc1;
+#pragma unroll
+  for (int q = 0; q < NTW; ++q) {
+    if (ta[q] >= 0) {
+      Gs[(ta[q] * 8 + g) * NB + tb[q] * 8 + 2 * t4] = acc[q][0];
+      Gs[(ta[q] * 8 + g) * NB + tb[q] * 8 + 2 * t4 + 1] = acc[q][1];
+    }
   }
   __syncthreads();
   if (w == 0) {
     // T (column-major) : T[i][i] = tau_i; T[0:i,i] = -tau_i T[0:i,0:i] G[0:i,i]
     double* Tp = a.T + ((int64_t)j * (a.K / NB) + P0 / NB) * NB * NB;
-    __shared__ double Tl[NB * NB];
+    double* Tl = S;  // the staging buffer is free once G is formed
     for (int i = 0; i < NB; ++i) {
       const double ti = tau_j[P0 + i];
       double z = 0.0;
