@@ -164,7 +164,7 @@ def launches_per_step(fs, iters):
         if K % 64 == 0:
             q = K // 64
             k2a = 4 * q + (q - 1)            # panel, wy32, panel, combine_t, wy64
-            k2c = q
+            k2c = 1 if os.environ.get("FEATLSQ_QFORM", "1") != "0" else q  # qform.cu: one fused launch
         else:
             k2a = npan + (npan - 1)
             k2c = npan
