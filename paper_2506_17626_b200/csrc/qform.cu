@@ -34,6 +34,25 @@ constexpr int NW = 16, NT = NW * 32;
 #define QF_STAGES 3
 #endif
 constexpr int STAGES = QF_STAGES;
+// timing experiments only: QF_NO_MMA / QF_NO_LOAD / QF_NO_SYNC drop the
+// products / the loads / the per-chunk barriers (results are then wrong)
+#ifdef QF_NO_MMA
+#define QF_MMA(d0, d1, a, b) ((d0) += (a) * 0.0 + (b) * 0.0)
+#else
+#define QF_MMA(d0, d1, a, b) fl::dmma(d0, d1, a, b)
+#endif
+#ifdef QF_NO_LOAD
+#define QF_LOAD(x) ((void)0)
+#else
+#define QF_LOAD(x) x
+#endif
+#ifdef QF_NO_SYNC
+#define QF_SYNC() ((void)0)
+#define QF_GSYNC(id) ((void)0)
+#else
+#define QF_SYNC() __syncthreads()
+#define QF_GSYNC(id) asm volatile("bar.sync %0, 128;\n" ::"r"(id) : "memory")
+#endif
 constexpr int VST = 2 * NB * LDS;  // doubles per V stage: V_{b-1} columns 0..63, V_b columns 64..127
 constexpr int CST = TN * LDS;
 constexpr size_t RING = (size_t)STAGES * (VST + CST) * sizeof(double);
@@ -86,13 +105,16 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
     srr[it] = (p % (RC / 2)) * 2;
   }
 
-  // phase-B warp tiles (W = V^T C, 64 x 64, rows split over two k groups)
-  const int kg = w / (NW / 2), wl = w % (NW / 2);
-  const int mb = wl % 4, nbk = wl / 4;
-  // phase-A warp tiles (C -= V W', 32 x 64): two m-tiles x one n-tile
-  const int mp = w % 2, nt = w / 2;
-
-  double acc[2][4][2];
+  // Register blocking sized for shared-memory traffic (both phases read
+  // their operands from the ring): phase A (C -= V W', 32 x 64) warp tile =
+  // one m-tile x two n-tiles with W' held in registers for the whole pass, so
+  // a V fragment feeds two DMMAs and W' is never re-read (128 B of shared
+  // loads per DMMA); phase B (W = V^T C, 64 x 64) warp tile = 2 x 2 tiles
+  // over all of the chunk's rows (256 B per DMMA, no cross-warp reduction).
+  const int am = w % 4, an = 2 * (w / 4);
+  const int bm = 2 * (w % 4), bn = 2 * (w / 4);
+  double bw[NB / 4][2];  // W'(4k + t, 8 (an + n) + g)
+  double acc[2][2][2];
 
   int bA = -1, bB = nact - 1;
   for (;;) {
@@ -105,7 +127,7 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int n = 0; n < 4; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
+      for (int n = 0; n < 2; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
 
     auto load = [&](int ch) {
       const int rbase = rlo + ch * RC, s = ch % STAGES;
@@ -116,16 +138,16 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
         const int col = scol[it], rr = srr[it], row = rbase + rr;
         if (doB) {
           double* d = vs + col * LDS + rr;
-          if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bB + col) * vld + row);
+          if (row < vld) QF_LOAD(fl::cp_async16(d, V + (int64_t)(NB * bB + col) * vld + row));
           else d[0] = d[1] = 0.0;
         }
         if (doA) {
           double* d = vs + (NB + col) * LDS + rr;
-          if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bA + col) * vld + row);
+          if (row < vld) QF_LOAD(fl::cp_async16(d, V + (int64_t)(NB * bA + col) * vld + row));
           else d[0] = d[1] = 0.0;
         }
         double* d = cs + col * LDS + rr;
-        if (col < ncol && row < cz && row < cld) fl::cp_async16(d, C + (int64_t)col * cld + row);
+        if (col < ncol && row < cz && row < cld) QF_LOAD(fl::cp_async16(d, C + (int64_t)col * cld + row));
         else d[0] = d[1] = 0.0;
       }
     };
@@ -137,10 +159,13 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
     }
     for (int ch = 0; ch < nch; ++ch) {
       const int rbase = rlo + ch * RC;
+      // one CTA barrier per chunk: it publishes chunk ch and, since every
+      // warp has left chunk ch-1 when it arrives, frees that stage for the
+      // load issued right after it
+      fl::cp_async_wait<STAGES - 2>();
+      QF_SYNC();
       if (ch + STAGES - 1 < nch) load(ch + STAGES - 1);
       fl::cp_async_commit();
-      fl::cp_async_wait<STAGES - 1>();
-      __syncthreads();
       double* vs = Vs + (ch % STAGES) * VST;
       double* cs = Cs + (ch % STAGES) * CST;
       // unit lower-trapezoidal structure: V_b's diagonal starts at row 64 b
@@ -163,76 +188,64 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
       if (doA && rbase + RC > NB * bA) {
         const double* vb = vs + NB * LDS;
         double c[2][2];
+        const int row = am * 8 + g;
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          const int row = (2 * mp + mi) * 8 + g, col = nt * 8 + 2 * t;
-          c[mi][0] = cs[col * LDS + row];
-          c[mi][1] = cs[(col + 1) * LDS + row];
+        for (int n = 0; n < 2; ++n) {
+          const int col = (an + n) * 8 + 2 * t;
+          c[n][0] = cs[col * LDS + row];
+          c[n][1] = cs[(col + 1) * LDS + row];
         }
 #pragma unroll
         for (int k = 0; k < NB / 4; ++k) {
-          const double b = Wp[(4 * k + t) * LDW + nt * 8 + g];  // W'(4k + t, 8 nt + g)
+          const double av = -vb[(4 * k + t) * LDS + row];
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi)
-            fl::dmma(c[mi][0], c[mi][1], -vb[(4 * k + t) * LDS + (2 * mp + mi) * 8 + g], b);
+          for (int n = 0; n < 2; ++n) QF_MMA(c[n][0], c[n][1], av, bw[k][n]);
         }
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          const int row = (2 * mp + mi) * 8 + g, col = nt * 8 + 2 * t;
-          cs[col * LDS + row] = c[mi][0];
-          cs[(col + 1) * LDS + row] = c[mi][1];
+        for (int n = 0; n < 2; ++n) {
+          const int col = (an + n) * 8 + 2 * t;
+          cs[col * LDS + row] = c[n][0];
+          cs[(col + 1) * LDS + row] = c[n][1];
           if (rbase + row < mj) {
-            if (col < ncol) C[(int64_t)col * cld + rbase + row] = c[mi][0];
-            if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + rbase + row] = c[mi][1];
+            if (col < ncol) C[(int64_t)col * cld + rbase + row] = c[n][0];
+            if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + rbase + row] = c[n][1];
           }
         }
-        if (doB) __syncthreads();
+        // B below reads only C columns written by the 4 warps of this warp's
+        // group (an == bn): a named barrier over those 128 threads
+        if (doB) QF_GSYNC(1 + w / 4);
       }
       // ---- B: W_{b-1} += V_{b-1}^T C on the (updated) chunk ----
       if (doB) {
 #pragma unroll
-        for (int s = kg; s < RC / 4; s += 2) {
+        for (int s = 0; s < RC / 4; ++s) {
           const int k0 = 4 * s;
-          double av[2], bv[4];
+          double av[2], bv[2];
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((2 * mb + mi) * 8 + g) * LDS + k0 + t];
+          for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((bm + mi) * 8 + g) * LDS + k0 + t];
 #pragma unroll
-          for (int n = 0; n < 4; ++n) bv[n] = cs[((4 * nbk + n) * 8 + g) * LDS + k0 + t];
+          for (int n = 0; n < 2; ++n) bv[n] = cs[((bn + n) * 8 + g) * LDS + k0 + t];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) fl::dmma(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
+            for (int n = 0; n < 2; ++n) QF_MMA(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
         }
       }
-      __syncthreads();  // the stage is refilled by a later iteration
     }
     if (!doB) break;
 
     // ---- between passes: W' = T_{b-1} W in the ring's memory, fragments to registers ----
     fl::cp_async_wait<0>();
     __syncthreads();
-    if (kg == 1) {
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          const int row = (2 * mb + mi) * 8 + g, col = (4 * nbk + n) * 8 + 2 * t;
-          Ws[row * LDW + col] = acc[mi][n][0];
-          Ws[row * LDW + col + 1] = acc[mi][n][1];
-        }
-    }
+      for (int n = 0; n < 2; ++n) {
+        const int row = (bm + mi) * 8 + g, col = (bn + n) * 8 + 2 * t;
+        Ws[row * LDW + col] = acc[mi][n][0];
+        Ws[row * LDW + col + 1] = acc[mi][n][1];
+      }
     for (int i = threadIdx.x; i < NB * NB; i += NT) Ts[i] = Tj[(int64_t)bB * NB * NB + i];
-    __syncthreads();
-    if (kg == 0) {
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          const int row = (2 * mb + mi) * 8 + g, col = (4 * nbk + n) * 8 + 2 * t;
-          Ws[row * LDW + col] += acc[mi][n][0];
-          Ws[row * LDW + col + 1] += acc[mi][n][1];
-        }
-    }
     __syncthreads();
     {
       const int mt = w % (NB / 8), ntb = (w / (NB / 8)) * 4;
@@ -253,6 +266,10 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
       }
     }
     __syncthreads();  // W' complete; the ring is reloaded by the next pass
+#pragma unroll
+    for (int k = 0; k < NB / 4; ++k)
+#pragma unroll
+      for (int n = 0; n < 2; ++n) bw[k][n] = Wp[(4 * k + t) * LDW + (an + n) * 8 + g];
     bA = bB;
     --bB;
   }
