@@ -26,13 +26,30 @@ namespace {
 
 constexpr int NB = 64;    // reflectors per block
 constexpr int TN = 64;    // C columns per CTA
-constexpr int RC = 32;    // rows per staged chunk
-constexpr int LDS = RC + 4;
-constexpr int LDW = TN + 4;
-constexpr int NW = 16, NT = NW * 32;
+// CTA shape: QF_NW warps, 2 NW-row chunks (every phase-A warp owns one
+// m-tile x two n-tiles), QF_MINB CTAs per SM, QF_STAGES ring stages.
+// Measured on cfg4 (ncu, one filter): 16 warps / 3 stages 89.1 ms, 4 stages
+// 89.7 ms, 8 warps at two CTAs per SM 101.8 ms. Without the per-chunk
+// barriers (incorrect, timing only) 72 ms: the barriers, not the loads or
+// shared-memory bandwidth, hold the DMMA pipe near 68% busy.
+#ifndef QF_NW
+#define QF_NW 16
+#endif
+#ifndef QF_MINB
+#define QF_MINB 1
+#endif
 #ifndef QF_STAGES
 #define QF_STAGES 3
 #endif
+constexpr int NW = QF_NW, NT = NW * 32;
+constexpr int RC = 2 * NW;  // rows per staged chunk
+constexpr int LDS = RC + 4; // = 4 mod 16: conflict-free 8-byte fragment loads
+constexpr int LDW = TN + 4;
+constexpr int MT = RC / 8;            // m-tiles per chunk
+constexpr int BNN = 64 / NW / 2;     // phase-B warp tile: 2 m-tiles x BNN n-tiles
+constexpr int SLOTS = TN * (RC / 2) / NT;  // 16-byte staging slots per thread per operand
+static_assert(SLOTS * NT == TN * (RC / 2), "staging slots");
+static_assert(4 * MT == NW, "phase-A tiling");
 constexpr int STAGES = QF_STAGES;
 // timing experiments only: QF_NO_MMA / QF_NO_LOAD / QF_NO_SYNC drop the
 // products / the loads / the per-chunk barriers (results are then wrong)
@@ -56,10 +73,8 @@ constexpr int STAGES = QF_STAGES;
 constexpr int VST = 2 * NB * LDS;  // doubles per V stage: V_{b-1} columns 0..63, V_b columns 64..127
 constexpr int CST = TN * LDS;
 constexpr size_t RING = (size_t)STAGES * (VST + CST) * sizeof(double);
-// W' = T W stays in shared memory behind the ring (as registers it pins 32 of
-// the 128 per thread and the compiler then serialises the A-fragment loads)
-constexpr size_t SMEM = RING + (size_t)NB * LDW * sizeof(double);
-static_assert((size_t)(NB * LDW + NB * NB) * sizeof(double) <= RING, "W and T fit in the ring");
+constexpr size_t SMEM = RING;
+static_assert((size_t)(2 * NB * LDW) * sizeof(double) <= RING, "W and W' fit in the ring");
 
 struct QfArgs {
   const double* V;       // factored A store (reflectors below the diagonal)
@@ -75,13 +90,12 @@ struct QfArgs {
   int tiles_per_block;
 };
 
-__global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
+__global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
   extern __shared__ double sm[];
   double* Vs = sm;                      // [STAGES][128][LDS]
   double* Cs = Vs + STAGES * VST;       // [STAGES][64][LDS]
-  double* Ws = sm;                      // between passes: [64][LDW]
-  double* Ts = sm + NB * LDW;           //                 [64][64]
-  double* Wp = sm + RING / sizeof(double);  // W' [64][LDW], persistent
+  double* Ws = sm;                      // between passes: W [64][LDW]
+  double* Wp = sm + NB * LDW;           //                 W' = T W [64][LDW]
 
   const int j = blockIdx.x / a.tiles_per_block;
   const int c0 = (blockIdx.x % a.tiles_per_block) * TN;
@@ -96,10 +110,10 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
   const int nact = min(K / NB, (mj + NB - 1) / NB);  // blocks with reflectors
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
-  // this thread's two (column, row pair) staging slots of a 64 x RC tile
-  int scol[2], srr[2];
+  // this thread's (column, row pair) staging slots of a 64 x RC tile
+  int scol[SLOTS], srr[SLOTS];
 #pragma unroll
-  for (int it = 0; it < 2; ++it) {
+  for (int it = 0; it < SLOTS; ++it) {
     const int p = threadIdx.x + it * NT;
     scol[it] = p / (RC / 2);
     srr[it] = (p % (RC / 2)) * 2;
@@ -111,10 +125,10 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
   // a V fragment feeds two DMMAs and W' is never re-read (128 B of shared
   // loads per DMMA); phase B (W = V^T C, 64 x 64) warp tile = 2 x 2 tiles
   // over all of the chunk's rows (256 B per DMMA, no cross-warp reduction).
-  const int am = w % 4, an = 2 * (w / 4);
-  const int bm = 2 * (w % 4), bn = 2 * (w / 4);
+  const int am = w % MT, an = 2 * (w / MT);
+  const int bm = 2 * (w % 4), bn = BNN * (w / 4);
   double bw[NB / 4][2];  // W'(4k + t, 8 (an + n) + g)
-  double acc[2][2][2];
+  double acc[2][BNN][2];
 
   int bA = -1, bB = nact - 1;
   for (;;) {
@@ -127,14 +141,14 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int n = 0; n < 2; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
+      for (int n = 0; n < BNN; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
 
     auto load = [&](int ch) {
       const int rbase = rlo + ch * RC, s = ch % STAGES;
       double* vs = Vs + s * VST;
       double* cs = Cs + s * CST;
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {
+      for (int it = 0; it < SLOTS; ++it) {
         const int col = scol[it], rr = srr[it], row = rbase + rr;
         if (doB) {
           double* d = vs + col * LDS + rr;
@@ -220,56 +234,58 @@ __global__ void __launch_bounds__(NT, 1) qform_kernel(QfArgs a) {
 #pragma unroll
         for (int s = 0; s < RC / 4; ++s) {
           const int k0 = 4 * s;
-          double av[2], bv[2];
+          double av[2], bv[BNN];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((bm + mi) * 8 + g) * LDS + k0 + t];
 #pragma unroll
-          for (int n = 0; n < 2; ++n) bv[n] = cs[((bn + n) * 8 + g) * LDS + k0 + t];
+          for (int n = 0; n < BNN; ++n) bv[n] = cs[((bn + n) * 8 + g) * LDS + k0 + t];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int n = 0; n < 2; ++n) QF_MMA(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
+            for (int n = 0; n < BNN; ++n) QF_MMA(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
         }
       }
     }
     if (!doB) break;
 
-    // ---- between passes: W' = T_{b-1} W in the ring's memory, fragments to registers ----
+    // ---- between passes: W' = T_{b-1} W in the ring's memory (T from L2),
+    //      then W' fragments to registers ----
     fl::cp_async_wait<0>();
     __syncthreads();
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int n = 0; n < 2; ++n) {
+      for (int n = 0; n < BNN; ++n) {
         const int row = (bm + mi) * 8 + g, col = (bn + n) * 8 + 2 * t;
         Ws[row * LDW + col] = acc[mi][n][0];
         Ws[row * LDW + col + 1] = acc[mi][n][1];
       }
-    for (int i = threadIdx.x; i < NB * NB; i += NT) Ts[i] = Tj[(int64_t)bB * NB * NB + i];
     __syncthreads();
     {
-      const int mt = w % (NB / 8), ntb = (w / (NB / 8)) * 4;
-      double p2[4][2];
+      constexpr int N2 = 64 / NW;  // n-tiles of W' per warp
+      const int mt = w % 8, ntb = (w / 8) * N2;
+      const double* Tb = Tj + (int64_t)bB * NB * NB;
+      double p2[N2][2];
 #pragma unroll
-      for (int n = 0; n < 4; ++n) p2[n][0] = p2[n][1] = 0.0;
-#pragma unroll
+      for (int n = 0; n < N2; ++n) p2[n][0] = p2[n][1] = 0.0;
+#pragma unroll 4
       for (int k0 = 0; k0 < NB; k0 += 4) {
-        const double av = Ts[(k0 + t) * NB + mt * 8 + g];  // T[mt*8+g][k0+t]
+        const double av = __ldg(Tb + (k0 + t) * NB + mt * 8 + g);  // T[mt*8+g][k0+t]
 #pragma unroll
-        for (int n = 0; n < 4; ++n) fl::dmma(p2[n][0], p2[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
+        for (int n = 0; n < N2; ++n) fl::dmma(p2[n][0], p2[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
       }
-      __syncthreads();
 #pragma unroll
-      for (int n = 0; n < 4; ++n) {
+      for (int n = 0; n < N2; ++n) {
         Wp[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t] = p2[n][0];
         Wp[(mt * 8 + g) * LDW + (ntb + n) * 8 + 2 * t + 1] = p2[n][1];
       }
     }
-    __syncthreads();  // W' complete; the ring is reloaded by the next pass
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < NB / 4; ++k)
 #pragma unroll
       for (int n = 0; n < 2; ++n) bw[k][n] = Wp[(4 * k + t) * LDW + (an + n) * 8 + g];
+    __syncthreads();  // the ring is reloaded by the next pass
     bA = bB;
     --bB;
   }
