@@ -51,25 +51,6 @@ constexpr int SLOTS = TN * (RC / 2) / NT;  // 16-byte staging slots per thread p
 static_assert(SLOTS * NT == TN * (RC / 2), "staging slots");
 static_assert(4 * MT == NW, "phase-A tiling");
 constexpr int STAGES = QF_STAGES;
-// timing experiments only: QF_NO_MMA / QF_NO_LOAD / QF_NO_SYNC drop the
-// products / the loads / the per-chunk barriers (results are then wrong)
-#ifdef QF_NO_MMA
-#define QF_MMA(d0, d1, a, b) ((d0) += (a) * 0.0 + (b) * 0.0)
-#else
-#define QF_MMA(d0, d1, a, b) fl::dmma(d0, d1, a, b)
-#endif
-#ifdef QF_NO_LOAD
-#define QF_LOAD(x) ((void)0)
-#else
-#define QF_LOAD(x) x
-#endif
-#ifdef QF_NO_SYNC
-#define QF_SYNC() ((void)0)
-#define QF_GSYNC(id) ((void)0)
-#else
-#define QF_SYNC() __syncthreads()
-#define QF_GSYNC(id) asm volatile("bar.sync %0, 128;\n" ::"r"(id) : "memory")
-#endif
 constexpr int VST = 2 * NB * LDS;  // doubles per V stage: V_{b-1} columns 0..63, V_b columns 64..127
 constexpr int CST = TN * LDS;
 constexpr size_t RING = (size_t)STAGES * (VST + CST) * sizeof(double);
@@ -130,6 +111,17 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
   double bw[NB / 4][2];  // W'(4k + t, 8 (an + n) + g)
   double acc[2][BNN][2];
 
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      fl::mbar_init(&full[i], NT);   // one cp.async arrival per thread
+      fl::mbar_init(&empty[i], NW);  // one arrival per warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  int G0 = 0;
+
   int bA = -1, bB = nact - 1;
   for (;;) {
     const bool doA = bA >= 0, doB = bB >= 0;
@@ -143,45 +135,45 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
 #pragma unroll
       for (int n = 0; n < BNN; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
 
-    auto load = [&](int ch) {
-      const int rbase = rlo + ch * RC, s = ch % STAGES;
-      double* vs = Vs + s * VST;
-      double* cs = Cs + s * CST;
+    // every thread stages its slots of chunk ch into ring stage st and arrives
+    // on full[st] when its copies land (out-of-range rows are zero-filled by
+    // the same async unit, so one wait on full[st] covers all of the stage)
+    auto load = [&](int ch, int st) {
+      const int rbase = rlo + ch * RC;
+      double* vs = Vs + st * VST;
+      double* cs = Cs + st * CST;
 #pragma unroll
       for (int it = 0; it < SLOTS; ++it) {
         const int col = scol[it], rr = srr[it], row = rbase + rr;
         if (doB) {
           double* d = vs + col * LDS + rr;
-          if (row < vld) QF_LOAD(fl::cp_async16(d, V + (int64_t)(NB * bB + col) * vld + row));
-          else d[0] = d[1] = 0.0;
+          if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bB + col) * vld + row);
+          else fl::cp_async16_zero(d, V);
         }
         if (doA) {
           double* d = vs + (NB + col) * LDS + rr;
-          if (row < vld) QF_LOAD(fl::cp_async16(d, V + (int64_t)(NB * bA + col) * vld + row));
-          else d[0] = d[1] = 0.0;
+          if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bA + col) * vld + row);
+          else fl::cp_async16_zero(d, V);
         }
         double* d = cs + col * LDS + rr;
-        if (col < ncol && row < cz && row < cld) QF_LOAD(fl::cp_async16(d, C + (int64_t)col * cld + row));
-        else d[0] = d[1] = 0.0;
+        if (col < ncol && row < cz && row < cld) fl::cp_async16(d, C + (int64_t)col * cld + row);
+        else fl::cp_async16_zero(d, C);
       }
+      fl::cp_async_arrive(&full[st]);
     };
 
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nch) load(s);
-      fl::cp_async_commit();
-    }
+    // Chunks are numbered across passes (G); chunk G uses stage G % STAGES
+    // for the (G / STAGES)-th time, so both barriers of that stage complete
+    // their phase of parity (G / STAGES) & 1 for it. No CTA barrier per
+    // chunk: a warp waits for its chunk's data (full) and, before refilling a
+    // stage, for every warp to have left it (empty), which is a chunk later.
+    for (int c = 0; c < STAGES - 1 && c < nch; ++c) load(c, (G0 + c) % STAGES);
     for (int ch = 0; ch < nch; ++ch) {
+      const int G = G0 + ch, st = G % STAGES;
       const int rbase = rlo + ch * RC;
-      // one CTA barrier per chunk: it publishes chunk ch and, since every
-      // warp has left chunk ch-1 when it arrives, frees that stage for the
-      // load issued right after it
-      fl::cp_async_wait<STAGES - 2>();
-      QF_SYNC();
-      if (ch + STAGES - 1 < nch) load(ch + STAGES - 1);
-      fl::cp_async_commit();
-      double* vs = Vs + (ch % STAGES) * VST;
-      double* cs = Cs + (ch % STAGES) * CST;
+      fl::mbar_wait(&full[st], (G / STAGES) & 1);
+      double* vs = Vs + st * VST;
+      double* cs = Cs + st * CST;
       // unit lower-trapezoidal structure: V_b's diagonal starts at row 64 b
       const bool mB = doB && rbase < NB * bB + NB, mA = doA && rbase < NB * bA + NB;
       if (mB || mA) {
@@ -213,7 +205,7 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
         for (int k = 0; k < NB / 4; ++k) {
           const double av = -vb[(4 * k + t) * LDS + row];
 #pragma unroll
-          for (int n = 0; n < 2; ++n) QF_MMA(c[n][0], c[n][1], av, bw[k][n]);
+          for (int n = 0; n < 2; ++n) fl::dmma(c[n][0], c[n][1], av, bw[k][n]);
         }
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
@@ -227,7 +219,7 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
         }
         // B below reads only C columns written by the 4 warps of this warp's
         // group (an == bn): a named barrier over those 128 threads
-        if (doB) QF_GSYNC(1 + w / 4);
+        if (doB) asm volatile("bar.sync %0, 128;\n" ::"r"(1 + w / 4) : "memory");
       }
       // ---- B: W_{b-1} += V_{b-1}^T C on the (updated) chunk ----
       if (doB) {
@@ -242,10 +234,20 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int n = 0; n < BNN; ++n) QF_MMA(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
+            for (int n = 0; n < BNN; ++n) fl::dmma(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
         }
       }
+      __syncwarp();
+      if (lane == 0) fl::mbar_arrive(&empty[st]);
+      if (ch + STAGES - 1 < nch) {
+        // stage of chunk ch + STAGES - 1 = stage of chunk ch - 1 (free before
+        // this pass when ch == 0: the passes are separated by a CTA barrier)
+        const int sn = (G + STAGES - 1) % STAGES;
+        if (ch >= 1) fl::mbar_wait(&empty[sn], ((G - 1) / STAGES) & 1);
+        load(ch + STAGES - 1, sn);
+      }
     }
+    G0 += nch;
     if (!doB) break;
 
     // ---- between passes: W' = T_{b-1} W in the ring's memory (T from L2),
