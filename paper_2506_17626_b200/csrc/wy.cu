@@ -2,7 +2,8 @@
 //
 // Template NB in {32, 64} (reflectors per block), 8*NB/32 warps per CTA.
 // One CTA owns one (block, TN-column tile) and streams the rows in RC-row
-// chunks through a 3-stage cp.async pipeline, twice: phase 1 accumulates
+// chunks through a cp.async ring (full/empty mbarriers, no CTA barrier per
+// chunk), twice: phase 1 accumulates
 // W = V^T C (NB x TN) with the k (row) dimension split over two warp groups
 // (each warp: 2 x 4 mma tiles, 6 fragment loads per 8 DMMA), phase 2 forms
 // W' = op(T) W, phase 3 updates C -= V W' with W' held in registers and
@@ -39,13 +40,13 @@ __device__ __forceinline__ void load_chunk(const double* __restrict__ V, int vld
     const int col = p / (RC / 2), rr = (p % (RC / 2)) * 2, row = rbase + rr;
     double* dst = vs + col * LDS + rr;
     if (row < vld) fl::cp_async16(dst, V + (int64_t)col * vld + row);
-    else dst[0] = dst[1] = 0.0;
+    else fl::cp_async16_zero(dst, V);
   }
   for (int p = threadIdx.x; p < TN * (RC / 2); p += NT) {
     const int col = p / (RC / 2), rr = (p % (RC / 2)) * 2, row = rbase + rr;
     double* dst = cs + col * LDS + rr;
     if (col < ncol && row < cld) fl::cp_async16(dst, C + (int64_t)col * cld + row);
-    else dst[0] = dst[1] = 0.0;
+    else fl::cp_async16_zero(dst, C);
   }
 }
 
@@ -101,22 +102,55 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int n = 0; n < 4; ++n) acc[mi][n][0] = acc[mi][n][1] = 0.0;
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nchunks) load_chunk<NB>(V, vld, C, cld, ncol, r0 + s * RC, stage_v(s), stage_c(s));
-    fl::cp_async_commit();
+  // full/empty mbarrier ring (no CTA barrier per chunk): chunk G of the
+  // kernel (phase 1 then phase 3 numbering) uses stage G % STAGES for the
+  // (G / STAGES)-th time; both barriers of the stage complete the phase of
+  // parity (G / STAGES) & 1 for it
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      fl::mbar_init(&full[i], Cfg<NB>::NT);
+      fl::mbar_init(&empty[i], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int nx = ch + STAGES - 1;
-    if (nx < nchunks)
-      load_chunk<NB>(V, vld, C, cld, ncol, r0 + nx * RC, stage_v(nx % STAGES), stage_c(nx % STAGES));
-    fl::cp_async_commit();
-    fl::cp_async_wait<STAGES - 1>();
-    __syncthreads();
-    if (ch * RC < NB) {
-      mask_unit<NB>(stage_v(ch % STAGES), ch * RC);
+  __syncthreads();
+  auto load = [&](int ch, int G) {
+    const int st = G % STAGES;
+    load_chunk<NB>(V, vld, C, cld, ncol, r0 + ch * RC, stage_v(st), stage_c(st));
+    fl::cp_async_arrive(&full[st]);
+  };
+  // chunk G's data: wait, then the unit-trapezoid mask on the first chunks
+  auto acquire = [&](int ch, int G) {
+    const int st = G % STAGES;
+    fl::mbar_wait(&full[st], (G / STAGES) & 1);
+    if (ch * RC < NB) {  // (every copy of the stage has landed once full[st] completes)
+      mask_unit<NB>(stage_v(st), ch * RC);
       __syncthreads();
     }
+  };
+  // leave chunk G's stage and refill it with chunk ch + STAGES - 1 of this pass
+  auto release = [&](int ch, int G, int n, int Gbase) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) fl::mbar_arrive(&empty[G % STAGES]);
+    const int nx = ch + STAGES - 1;
+    if (nx < n) {
+      const int Gn = Gbase + nx, Gp = Gn - STAGES;  // previous user of the stage
+      if (Gp >= 0) fl::mbar_wait(&empty[Gn % STAGES], (Gp / STAGES) & 1);
+      load(nx, Gn);
+    }
+  };
+  auto prologue = [&](int n, int Gbase) {
+    for (int c = 0; c < STAGES - 1 && c < n; ++c) {
+      const int Gn = Gbase + c, Gp = Gn - STAGES;
+      if (Gp >= 0) fl::mbar_wait(&empty[Gn % STAGES], (Gp / STAGES) & 1);
+      load(c, Gn);
+    }
+  };
+
+  prologue(nchunks, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    acquire(ch, ch);
     const double* vs = stage_v(ch % STAGES);
     const double* cs = stage_c(ch % STAGES);
 #pragma unroll
@@ -132,8 +166,10 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
 #pragma unroll
         for (int n = 0; n < 4; ++n) fl::dmma(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
     }
-    __syncthreads();
+    release(ch, ch, nchunks, 0);
   }
+  // phase 3's first chunks stream in while W is reduced and multiplied by T
+  prologue(nchunks, nchunks);
   if (kg == 1) {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
@@ -143,11 +179,6 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
         Ws[row * LDW + col] = acc[mi][n][0];
         Ws[row * LDW + col + 1] = acc[mi][n][1];
       }
-  }
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nchunks) load_chunk<NB>(V, vld, C, cld, ncol, r0 + s * RC, stage_v(s), stage_c(s));
-    fl::cp_async_commit();
   }
   __syncthreads();
   if (kg == 0) {
@@ -193,19 +224,11 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
 #pragma unroll
     for (int n = 0; n < NN; ++n) bw[k][n] = Ws[(4 * k + t) * LDW + (ncb + n) * 8 + g];
   for (int ch = 0; ch < nchunks; ++ch) {
-    const int nx = ch + STAGES - 1;
+    const int G = nchunks + ch;
     const int rbase = r0 + ch * RC;
-    if (nx < nchunks)
-      load_chunk<NB>(V, vld, C, cld, ncol, r0 + nx * RC, stage_v(nx % STAGES), stage_c(nx % STAGES));
-    fl::cp_async_commit();
-    fl::cp_async_wait<STAGES - 1>();
-    __syncthreads();
-    if (ch * RC < NB) {
-      mask_unit<NB>(stage_v(ch % STAGES), ch * RC);
-      __syncthreads();
-    }
-    const double* vs = stage_v(ch % STAGES);
-    double* cs = stage_c(ch % STAGES);
+    acquire(ch, G);
+    const double* vs = stage_v(G % STAGES);
+    const double* cs = stage_c(G % STAGES);
     double c[NN][2];
 #pragma unroll
     for (int n = 0; n < NN; ++n) {
@@ -231,7 +254,7 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
         }
       }
     }
-    __syncthreads();  // the stage is refilled by a later iteration's cp.async
+    release(ch, G, nchunks, nchunks);
   }
 }
 
