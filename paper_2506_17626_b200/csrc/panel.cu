@@ -69,62 +69,87 @@ struct PanelArgs {
 template <int W>
 __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double* Tw, double* tau_j, int col0) {
   // S: W columns of Mq rows (column-major, stride Mq), rows relative to col0.
-  for (int i = 0; i < W; ++i) {
-    double* si = S + i * Mq;
-    double part[1] = {0.0};
-    for (int r = i + 1 + threadIdx.x; r < Mq; r += NT) part[0] += si[r] * si[r];
-    const double alpha = si[i];
-    block_sums<1>(part, red, sc);
+  // One pass over the rows per column: the pass that applies H_s to the
+  // columns right of s also accumulates, for column s+1, its squared norm
+  // and its UNSCALED dots x^T S[k] with the columns right of it and with the
+  // earlier reflectors (rows > s+1). After one CTA reduction every thread
+  // forms dlarfg's beta, tau and scal = 1 / (alpha - beta) itself, and the
+  // dots of the scaled reflector as S[k][s+1] + scal * dot (the row-(s+1)
+  // term, v = 1, stashed by the row's owner). Rows are owned by thread
+  // r mod NT throughout, so each pass only reads values its own thread wrote.
+  __shared__ double rowb[2][W];
+  double acc[2 * W];
+  auto accumulate = [&](int s1, int r) {  // rows r > s1 of column s1 (updated)
+    const double x = S[s1 * Mq + r];
+    acc[0] += x * x;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      if (k > s1) acc[k] += x * S[k * Mq + r];
+      if (k < s1) acc[W + k] += x * S[k * Mq + r];  // reflector k (r > s1 > k: stored)
+    }
+  };
+  auto stash = [&](int s1) {  // row s1 of every column, by its owner
+#pragma unroll
+    for (int k = 0; k < W; ++k) rowb[s1 & 1][k] = S[k * Mq + s1];
+  };
+#pragma unroll
+  for (int k = 0; k < 2 * W; ++k) acc[k] = 0.0;
+  for (int r = threadIdx.x; r < Mq; r += NT) {
+    if (r > 0) accumulate(0, r);
+    else stash(0);
+  }
+  for (int s = 0; s < W; ++s) {
+    block_sums<2 * W>(acc, red, sc);
+    const double* rb = rowb[s & 1];
+    const double alpha = rb[s];
     const double xnorm = sqrt(sc[0]);
-    double beta, t;
+    double beta, t, scal;
     if (xnorm == 0.0) {
       t = 0.0;
       beta = alpha;
+      scal = 1.0;
     } else {
       beta = -copysign(hypot(alpha, xnorm), alpha);
       t = (beta - alpha) / beta;
-      const double scal = 1.0 / (alpha - beta);
-      for (int r = i + 1 + threadIdx.x; r < Mq; r += NT) si[r] *= scal;
+      scal = 1.0 / (alpha - beta);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      si[i] = beta;
-      tau_j[col0 + i] = t;
-      Tw[i * W + i] = t;
-    }
-    __syncthreads();
-    // dots of v_i with the remaining inner columns and with the previous reflectors
-    double p[2 * W];
+    double pk[W];  // t * v_s^T S[k] for k > s
 #pragma unroll
-    for (int k = 0; k < 2 * W; ++k) p[k] = 0.0;
-    for (int r = i + threadIdx.x; r < Mq; r += NT) {
-      const double v = (r == i) ? 1.0 : si[r];
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        if (k > i) p[k] += v * S[k * Mq + r];
-        if (k < i) {  // previous reflector k: v_k[r] (r > i > k, so stored)
-          p[W + k] += v * S[k * Mq + r];
-        }
-      }
-    }
-    block_sums<2 * W>(p, red, sc);
-    // T column i (dlarft forward, columnwise): T[0:i, i] = -t * T[0:i,0:i] * (V_prev^T v_i)
-    if (threadIdx.x < i) {
+    for (int k = 0; k < W; ++k) pk[k] = (k > s) ? t * (rb[k] + scal * sc[k]) : 0.0;
+    // T column s (dlarft forward, columnwise): T[0:s, s] = -t T[0:s,0:s] (V_prev^T v_s)
+    if (threadIdx.x < s) {
       const int a = threadIdx.x;
       double z = 0.0;
-      for (int b = a; b < i; ++b) z += Tw[b * W + a] * sc[W + b];
-      Tw[i * W + a] = -t * z;
+      for (int b = a; b < s; ++b) z += Tw[b * W + a] * (rb[b] + scal * sc[W + b]);
+      Tw[s * W + a] = -t * z;
     }
-    // apply H_i to the remaining inner columns
-    if (t != 0.0) {
-      for (int k = i + 1; k < W; ++k) {
-        const double d = t * sc[k];
-        double* sk = S + k * Mq;
-        for (int r = i + threadIdx.x; r < Mq; r += NT) sk[r] -= d * ((r == i) ? 1.0 : si[r]);
+    if (threadIdx.x == 0) {
+      tau_j[col0 + s] = t;
+      Tw[s * W + s] = t;
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * W; ++k) acc[k] = 0.0;
+    for (int r = threadIdx.x; r < Mq; r += NT) {
+      if (r < s) continue;
+      double v = 1.0;
+      if (r == s) {
+        S[s * Mq + s] = beta;
+      } else {
+        v = S[s * Mq + r] * scal;
+        S[s * Mq + r] = v;
+      }
+      if (t != 0.0) {
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          if (k > s) S[k * Mq + r] -= pk[k] * v;
+      }
+      if (s + 1 < W) {
+        if (r > s + 1) accumulate(s + 1, r);
+        else if (r == s + 1) stash(s + 1);
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 template <int W>
