@@ -40,6 +40,12 @@ constexpr int NW = NT / 32;
 #ifndef QRCP_EARLY_CLOSE
 #define QRCP_EARLY_CLOSE 0  // 1: dlaqps's literal early panel close on a flagged norm
 #endif
+#ifndef QRCP_PREFETCH
+// 1: bulk L2 prefetch of the step's trailing columns behind the argmax.
+// Measured on cfg4: 115.7 vs 89.6 ms, DRAM reads 627 vs 376 GB (the lines
+// are evicted again before the gemv reaches them at 296 blocks in flight)
+#define QRCP_PREFETCH 0
+#endif
 #ifndef QRCP_MB
 #define QRCP_MB 2
 #endif
@@ -132,6 +138,16 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             bv = x;
             bi = c;
           }
+#if QRCP_PREFETCH
+          // the step's F-gemv streams rows i0..M-1 of every trailing column:
+          // start pulling them into L2 now, behind the argmax, swap and dlarfg
+          if (i + 1 < M) {
+            const int i0 = i & ~1;
+            const unsigned bytes = (unsigned)(((M - i0) * 8 + 15) & ~15);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(A + (int64_t)c * K + i0), "r"(bytes)
+                         : "memory");
+          }
+#endif
         }
         argmax_lowest(bv, bi);
         if (lane == 0) {
