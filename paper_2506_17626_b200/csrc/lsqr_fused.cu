@@ -38,6 +38,12 @@
 
 #include "common.cuh"
 
+#ifndef FL_PARTIAL_EVICT_LAST
+// 1: partial-product stores with an L2 evict_last policy (for the row
+// kernel's gather). Measured on cfg4: 1.416 vs 1.399 ms per iteration: off.
+#define FL_PARTIAL_EVICT_LAST 0
+#endif
+
 namespace {
 
 // shared memory per CTA with MB CTAs resident per SM: 227 KB for one, else
@@ -262,12 +268,26 @@ __global__ void __launch_bounds__(NT, MB)
         }
       }
     }
+#if FL_PARTIAL_EVICT_LAST
+    // the row kernel gathers these right after this kernel: keep them in L2
+    // while the Q stream passes through
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+#endif
 #pragma unroll
     for (int i = 0; i < RP; ++i) {
       const int r = 2 * (threadIdx.x + i * NT);
       double* pout = op.partial + h * op.partial_len + op.row_off[j];
+#if FL_PARTIAL_EVICT_LAST
+      if (r < m)
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(pout + r), "d"(pp_r[i].x), "l"(pol) : "memory");
+      if (r + 1 < m)
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(pout + r + 1), "d"(pp_r[i].y), "l"(pol)
+                     : "memory");
+#else
       if (r < m) pout[r] = pp_r[i].x;
       if (r + 1 < m) pout[r + 1] = pp_r[i].y;
+#endif
     }
   }
   // ---- grid reductions: alpha^2, w^2, non-finite ----
