@@ -38,6 +38,9 @@
 
 #include "common.cuh"
 
+#ifndef ROW_CTAS_PER_SM
+#define ROW_CTAS_PER_SM 4
+#endif
 #ifndef FL_PARTIAL_EVICT_LAST
 // 1: partial-product stores with an L2 evict_last policy (for the row
 // kernel's gather). Measured on cfg4: 1.416 vs 1.399 ms per iteration: off.
@@ -406,15 +409,53 @@ __global__ void __launch_bounds__(256) row_kernel(fl_blockop op, fl_lsqr_vecs ve
   const double tr = st->theta / st->rho;  // rho here is rho_{it-1}
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
   double ss = 0.0;
-  for (int g = gtid; g < op.nrows; g += gsz) {
-    double acc = 0.0;
-    for (int e = op.gptr[g]; e < op.gptr[g + 1]; ++e) {
-      const int64_t src = op.gsrc[e];
-      for (int h = 0; h < S; ++h) acc += op.partial[h * op.partial_len + src];
+  // The gather is a chain of dependent loads (gptr -> gsrc -> partial): the
+  // next row's gptr pair and u are fetched while this row's sources are in
+  // flight, and a row's sources (4 at a time) and their partials are loaded
+  // before any is summed. Same summation order as one source at a time.
+  constexpr int ME = 4;
+  int g = gtid;
+  int e0 = 0, e1 = 0;
+  double ug = 0.0;
+  if (g < op.nrows) {
+    e0 = op.gptr[g];
+    e1 = op.gptr[g + 1];
+    ug = vec.u[g];
+  }
+  while (g < op.nrows) {
+    const int gn = g + gsz;
+    int n0 = 0, n1 = 0;
+    double un_next = 0.0;
+    if (gn < op.nrows) {
+      n0 = op.gptr[gn];
+      n1 = op.gptr[gn + 1];
+      un_next = vec.u[gn];
     }
-    const double un = acc / alpha - alpha * (vec.u[g] / bprev);
+    double acc = 0.0;
+    for (int eb = e0; eb < e1; eb += ME) {
+      int64_t src[ME];
+#pragma unroll
+      for (int q = 0; q < ME; ++q) src[q] = (eb + q < e1) ? op.gsrc[eb + q] : 0;
+      double pv[ME][FL_LSQR_SPLIT_MAX];
+#pragma unroll
+      for (int q = 0; q < ME; ++q)
+#pragma unroll
+        for (int h = 0; h < FL_LSQR_SPLIT_MAX; ++h)
+          pv[q][h] = (eb + q < e1 && h < S) ? op.partial[h * op.partial_len + src[q]] : 0.0;
+#pragma unroll
+      for (int q = 0; q < ME; ++q)
+        if (eb + q < e1)
+#pragma unroll
+          for (int h = 0; h < FL_LSQR_SPLIT_MAX; ++h)
+            if (h < S) acc += pv[q][h];
+    }
+    const double un = acc / alpha - alpha * (ug / bprev);
     vec.u[g] = un;
     ss += un * un;
+    g = gn;
+    e0 = n0;
+    e1 = n1;
+    ug = un_next;
   }
   for (int64_t c = gtid; c < op.ncols_total; c += gsz) {
     const double vv = vec.vp[c] / alpha;  // v = v'/alpha (:141)
@@ -551,7 +592,7 @@ int fused(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t i
 int row_grid(const fl_blockop* op) {
   const int64_t n = op->nrows > op->ncols_total ? op->nrows : op->ncols_total;
   int64_t g = (n + 255) / 256;
-  if (g > 148 * 8) g = 148 * 8;
+  if (g > 148 * ROW_CTAS_PER_SM) g = 148 * ROW_CTAS_PER_SM;  // one wave (64 registers per thread)
   return (int)(g < 1 ? 1 : g);
 }
 
