@@ -307,6 +307,16 @@ int fl_dev_wy_apply(const double* V, const int64_t* voff, const int32_t* vld, do
                     int64_t tstride, int32_t nb, int32_t row0, int32_t transT, const int32_t* ncols,
                     const int32_t* tiles, int32_t ntiles, void* stream);
 
+/* Diagnostic (kernel-level tests): fused K2c over caller tables. Every block
+ * j: C_j (m_j x rank_j, holding [Q1_j; 0]) <- H_0 .. H_{K-1} C_j with the
+ * reflectors in V_j's K columns (unit diagonal implicit, entries on and above
+ * it ignored) applied as 64-wide compact-WY blocks whose T factors are
+ * T64[j][b] (64 x 64 column-major upper triangular); K % 64 == 0. Replaces
+ * dorgqr's Q formation (linalg.py:74) on route R. */
+int fl_dev_qform(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
+                 const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int32_t K,
+                 int32_t nblocks, void* stream);
+
 /* build metadata */
 const char* fl_version(void);
 /* description of the calling thread's last FL_ERR_CUDA ("file:line: name (text)") */

@@ -114,6 +114,7 @@ def lib():
                             C.c_double, vp, vp, vp, vp, vp, vp],
         "fl_dev_wy_apply": [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
                             C.c_int32, vp, vp, C.c_int32, vp],
+        "fl_dev_qform": [vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int32, vp],
         "fl_error_blocks": [C.POINTER(BlockOp), vp, vp, C.c_int32, C.POINTER(BlockOp), C.c_int32,
                             vp, vp],
         "fl_monitor_error": [C.POINTER(TestMonitor), vp, vp],
@@ -141,7 +142,7 @@ def lib():
 
 
 EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", "fl_lsqr_init",
-            "fl_lsqr_iterate", "fl_backsub_scatter", "fl_probe_fp64", "fl_dev_wy_apply",
+            "fl_lsqr_iterate", "fl_backsub_scatter", "fl_probe_fp64", "fl_dev_wy_apply", "fl_dev_qform",
             "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error",
             "fl_error_blocks", "fl_monitor_error", "fl_lsqr_iterate_monitored",
             "fl_lsqr_monitor_flush", "fl_cg_init", "fl_cg_iterate", "fl_cg_residual",

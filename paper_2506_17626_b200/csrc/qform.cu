@@ -312,3 +312,12 @@ int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const 
   return FL_OK;
 }
 }  // namespace fl
+
+// Diagnostic entry point: one fused K2c launch over caller-built block tables
+// (device pointers), for kernel-level tests.
+extern "C" int fl_dev_qform(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
+                            const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64,
+                            int32_t K, int32_t nblocks, void* stream) {
+  if (nblocks == 0) return FL_OK;
+  return fl::qform_fused(V, voff, vld, m, C, coff, cld, rank, T64, K, nblocks, (cudaStream_t)stream);
+}

@@ -62,3 +62,50 @@ def test_wy_apply_matches_numpy(dev, transT, row0, NB):
         # padding rows untouched (zero)
         pad = out[coff[j]:coff[j] + cld[j] * ncol].reshape(ncol, cld[j])[:, m:]
         assert np.all(pad == 0.0)
+
+
+@pytest.mark.parametrize("K", [128, 256])
+def test_qform_fused_matches_numpy(dev, K):
+    """K2c fused (qform.cu): C_j <- H_0 .. H_{K-1} [Q1_j; 0] as 64-wide compact-WY
+    blocks in reverse, against numpy block by block (incl. m_j < K and
+    partial ranks)."""
+    torch, D, _lib = dev
+    rng = np.random.default_rng(11 + K)
+    ms = [K + 37, 3 * K, K, K - 20, 2 * K + 5]
+    ranks = [K, K - 5, 70, K - 20, 1]
+    nb = K // 64
+    vbuf, voff, vld, vmats = _blocks(ms, K, rng=rng)
+    # C = [Q1; 0]: rows >= K (and >= rank columns' rows past m) zero
+    cbuf, coff, cld, cmats = _blocks(ms, K, rng=rng)
+    for j, m in enumerate(ms):
+        cmats[j][K:] = 0.0
+        blk = cbuf[coff[j]:coff[j] + cld[j] * K].reshape(K, cld[j])
+        blk[:, K:] = 0.0
+    T = np.stack([np.stack([np.triu(rng.standard_normal((64, 64))) * 0.1 for _ in range(nb)]) for _ in ms])
+    d = {k: D.to_dev(v) for k, v in dict(
+        V=vbuf, voff=voff, vld=vld, C=cbuf, coff=coff, cld=cld, m=np.array(ms, np.int32),
+        rank=np.array(ranks, np.int32),
+        T=np.ascontiguousarray(T.transpose(0, 1, 3, 2)).ravel()).items()}   # column-major per block
+    _lib.check(_lib.lib().fl_dev_qform(
+        D.ptr(d["V"]), D.ptr(d["voff"]), D.ptr(d["vld"]), D.ptr(d["m"]), D.ptr(d["C"]),
+        D.ptr(d["coff"]), D.ptr(d["cld"]), D.ptr(d["rank"]), D.ptr(d["T"]), K, len(ms),
+        D.stream_ptr()), "qform")
+    out = d["C"].cpu().numpy()
+    for j, (m, r) in enumerate(zip(ms, ranks)):
+        V = vmats[j].copy()
+        for c in range(K):  # entries on and above the diagonal are not the reflector's
+            V[:min(c, m), c] = 0.0
+            if c < m:
+                V[c, c] = 1.0
+        want = cmats[j].copy()
+        for b in range(nb - 1, -1, -1):
+            r0 = 64 * b
+            if r0 >= m:
+                continue
+            Vb = V[r0:, r0:r0 + 64]
+            want[r0:, :r] -= Vb @ (T[j, b] @ (Vb.T @ want[r0:, :r]))
+        got = out[coff[j]:coff[j] + cld[j] * K].reshape(K, cld[j])[:, :m].T
+        scale = max(1.0, np.abs(want).max())
+        assert np.abs(got[:, :r] - want[:, :r]).max() <= 1e-12 * scale, j
+        # columns past the rank are left as they were
+        assert np.array_equal(got[:, r:], cmats[j][:, r:]), j
