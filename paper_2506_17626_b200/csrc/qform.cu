@@ -69,6 +69,7 @@ struct QfArgs {
   const double* T64;     // (J, K/64, 64, 64) column-major upper-triangular T_b
   int K;
   int tiles_per_block;
+  const int32_t* nrefl;  // reflectors per block (null: all K); blocks past it are identities
 };
 
 __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
@@ -84,11 +85,14 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
   const int ncol = min(TN, a.rank[j] - c0);
   if (ncol <= 0 || mj <= 0) return;
   const int K = a.K;
-  const int vld = a.vld[j], cld = a.cld[j];
-  const double* V = a.V + a.voff[j];
-  double* C = a.C + a.coff[j] + (int64_t)c0 * cld;
+  // null offset / ld tables: dense (J, K, K) stores, ld K (the QRCP factor R0 and Q1)
+  const int vld = a.vld ? a.vld[j] : K, cld = a.cld ? a.cld[j] : K;
+  const double* V = a.V + (a.voff ? a.voff[j] : (int64_t)j * K * K);
+  double* C = a.C + (a.coff ? a.coff[j] : (int64_t)j * K * K) + (int64_t)c0 * cld;
   const double* Tj = a.T64 + (int64_t)j * (K / NB) * NB * NB;
-  const int nact = min(K / NB, (mj + NB - 1) / NB);  // blocks with reflectors
+  const int nr = a.nrefl ? min(a.nrefl[j], mj) : mj;
+  const int nact = min(K / NB, (nr + NB - 1) / NB);  // blocks with reflectors
+  if (nact <= 0) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
   // this thread's (column, row pair) staging slots of a 64 x RC tile
@@ -299,14 +303,14 @@ namespace fl {
 // Q (blocks at coff/cld, holding [Q1; 0]) <- Q0 Q for every block; K % 64 == 0.
 int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
                 const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int K, int J,
-                cudaStream_t s) {
+                cudaStream_t s, const int32_t* nrefl) {
   if (K % NB) return FL_ERR_INVALID;
   static bool attr = false;
   if (!attr) {
     FL_CUDA(cudaFuncSetAttribute(qform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr = true;
   }
-  QfArgs a{V, voff, vld, m, C, coff, cld, rank, T64, K, (K + TN - 1) / TN};
+  QfArgs a{V, voff, vld, m, C, coff, cld, rank, T64, K, (K + TN - 1) / TN, nrefl};
   qform_kernel<<<J * a.tiles_per_block, NT, SMEM, s>>>(a);
   FL_CHECK_LAUNCH();
   return FL_OK;
@@ -319,5 +323,6 @@ extern "C" int fl_dev_qform(const double* V, const int64_t* voff, const int32_t*
                             const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64,
                             int32_t K, int32_t nblocks, void* stream) {
   if (nblocks == 0) return FL_OK;
-  return fl::qform_fused(V, voff, vld, m, C, coff, cld, rank, T64, K, nblocks, (cudaStream_t)stream);
+  if (!voff || !vld || !coff || !cld) return FL_ERR_INVALID;
+  return fl::qform_fused(V, voff, vld, m, C, coff, cld, rank, T64, K, nblocks, (cudaStream_t)stream, nullptr);
 }

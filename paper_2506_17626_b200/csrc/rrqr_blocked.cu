@@ -28,7 +28,7 @@ int wy_nb();
 int wy_tn();
 int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
                 const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int K, int J,
-                cudaStream_t s);
+                cudaStream_t s, const int32_t* nrefl = nullptr);
 }  // namespace fl
 
 namespace {
@@ -163,10 +163,12 @@ __global__ void __launch_bounds__(NT) combine_t_kernel(const double* __restrict_
   __shared__ double V2s[NB * GLD];
   __shared__ double Xs[NB * NB];
   __shared__ double Ys[NB * NB];
+  if (q < 0) q = blockIdx.x;  // all 64-blocks in one launch
   const int j = blockIdx.y, P0 = 64 * q;
   const int npan32 = K / NB, npan64 = K / 64;
-  const double* A = W + off[j];
-  const int64_t ldj = ld[j];
+  // off / ld may be null: the (J, K, K) factor R0 (stride K * K, ld K)
+  const double* A = W + (off ? off[j] : (int64_t)j * K * K);
+  const int64_t ldj = ld ? ld[j] : K;
   const int M = m[j] - (P0 + NB);  // rows of V2's support
   const double* T1 = T32 + ((int64_t)j * npan32 + 2 * q) * NB * NB;
   const double* T2 = T1 + NB * NB;
@@ -237,7 +239,7 @@ __global__ void clamp_tau_kernel(double* tau, int K, const int32_t* rank) {
 
 namespace {
 struct Workspace {
-  double *fac, *R0, *Q1, *T0, *T1, *T64, *tau0, *tau1;
+  double *fac, *R0, *Q1, *T0, *T1, *T64, *T164, *tau0, *tau1;
   int32_t* kmax;
 };
 
@@ -257,6 +259,7 @@ Workspace carve(void* base, int J, int K, int64_t store_elems, size_t* total) {
   ws.T0 = (double*)take((size_t)J * npan * NB * NB * 8);
   ws.T1 = (double*)take((size_t)J * npan * NB * NB * 8);
   ws.T64 = (double*)take((size_t)J * (K / 64 + 1) * 64 * 64 * 8);
+  ws.T164 = (double*)take((size_t)J * (K / 64) * 64 * 64 * 8);  // 64-wide T of the QRCP reflectors
   ws.tau0 = (double*)take((size_t)J * K * 8);
   ws.tau1 = (double*)take((size_t)J * K * 8);
   ws.kmax = (int32_t*)take((size_t)J * 4);
@@ -350,7 +353,29 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
   build_t_kernel<<<dim3(npan, J), NT, 0, s>>>(ws.R0, K, ws.kmax, ws.tau1, rank, ws.T1);
   init_q1_r_kernel<<<dim3(64, J), 256, 0, s>>>(ws.R0, K, rank, ws.Q1, R);
   FL_CHECK_LAUNCH();
-  // ---- Q1 = H'_0 .. H'_{r-1} [S; 0]: panels in reverse, columns >= P0 only ----
+  // ---- Q1 = H'_0 .. H'_{r-1} [S; 0] ----
+  static const int qf = [] {
+    const char* e = getenv("FEATLSQ_QFORM");  // 0: two-pass wy_apply per reflector block
+    return e ? atoi(e) : 1;
+  }();
+  static const int qf1 = [] {
+    const char* e = getenv("FEATLSQ_QFORM_Q1");
+    return e ? atoi(e) : 0;
+  }();
+  if (wide && qf1) {
+    // opt-in: 64-wide T of the QRCP reflectors, then the fused sweep
+    // (qform.cu) over the first ceil(r / 64) reflector blocks only (tau is 0
+    // past the rank). Measured on cfg4: 12.7 ms per filter (combine 1.3 +
+    // sweep 11.4) against 8.5 for the 32-wide two-pass launches on these
+    // 512-row blocks, whose passes are too short for the fused kernel.
+    // Covered by the parity tests when enabled (82 passed).
+    combine_t_kernel<<<dim3(K / 64, J), NT, 0, s>>>(ws.R0, nullptr, nullptr, ws.kmax, K, ws.T1, ws.T164, -1);
+    FL_CHECK_LAUNCH();
+    if ((e = fl::qform_fused(ws.R0, nullptr, nullptr, ws.kmax, ws.Q1, nullptr, nullptr, rank, ws.T164, K, J, s,
+                             rank)))
+      return e;
+  } else
+  // panels in reverse, columns >= P0 only
   for (int p = npan - 1; p >= 0; --p) {
     const int P0 = p * NB;
     fl::WyArgs a{};
@@ -376,10 +401,6 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
   // ---- K2c: Qhat = Q0 [Q1; 0], reflector blocks of Q0 in reverse ----
   init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, (double*)Q->vals);
   FL_CHECK_LAUNCH();
-  static const int qf = [] {
-    const char* e = getenv("FEATLSQ_QFORM");  // 0: two-pass wy_apply per reflector block
-    return e ? atoi(e) : 1;
-  }();
   if (wide && qf) return fl::qform_fused(fac, A->off, A->ld, A->m, (double*)Q->vals, Q->off, Q->ld, rank, ws.T64, K, J, s);
   const int wb = wide ? 64 : NB;
   for (int p = K / wb - 1; p >= 0; --p) {
