@@ -176,18 +176,33 @@ __global__ void __launch_bounds__(NT) combine_t_kernel(const double* __restrict_
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
   // X = V1^T V2: 16 tiles of 8x8, 2 per warp
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  for (int r0 = 0; r0 < M; r0 += GC) {
-    for (int p = threadIdx.x; p < NB * GC; p += NT) {
-      const int col = p / GC, rr = p % GC, row = r0 + rr;  // row relative to P0 + 32
+  // the next chunk is loaded into registers while this one is multiplied
+  constexpr int PER = NB * GC / NT;
+  static_assert(PER * NT == NB * GC, "chunk must split evenly over the CTA");
+  double n1[PER], n2[PER];
+  auto fetch = [&](int r0) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int p = threadIdx.x + u * NT, col = p / GC, rr = p % GC, row = r0 + rr;  // row relative to P0 + 32
       double v1 = 0.0, v2 = 0.0;
       if (row < M) {
         v1 = A[(int64_t)(P0 + col) * ldj + P0 + NB + row];  // below V1's diagonal block
         if (row > col) v2 = A[(int64_t)(P0 + NB + col) * ldj + P0 + NB + row];
         else if (row == col) v2 = 1.0;
       }
-      V1s[col * GLD + rr] = v1;
-      V2s[col * GLD + rr] = v2;
+      n1[u] = v1;
+      n2[u] = v2;
     }
+  };
+  fetch(0);
+  for (int r0 = 0; r0 < M; r0 += GC) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int p = threadIdx.x + u * NT, col = p / GC, rr = p % GC;
+      V1s[col * GLD + rr] = n1[u];
+      V2s[col * GLD + rr] = n2[u];
+    }
+    if (r0 + GC < M) fetch(r0 + GC);
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
