@@ -137,15 +137,22 @@ __global__ void init_q1_r_kernel(const double* __restrict__ R0, int K, const int
 }
 
 // Qhat[j] (ld_j x K): rows < K, cols < r: Q1; everything else 0
+// Q store <- [Q1; 0]. sparse = 1 (fused K2c): only the first rank columns,
+// rows < K and the padding rows m..ld-1 are written; qform writes rows
+// K..m-1 itself and treats them as zero until then.
 __global__ void init_qhat_kernel(const double* __restrict__ Q1, int K, const int32_t* __restrict__ rank,
                                  const int64_t* __restrict__ off, const int32_t* __restrict__ ld,
-                                 double* __restrict__ Q) {
+                                 const int32_t* __restrict__ m, int sparse, double* __restrict__ Q) {
   const int j = blockIdx.y;
-  const int ldj = ld[j], rk = rank[j];
-  const int64_t n = (int64_t)ldj * K;
+  const int ldj = ld[j], rk = rank[j], mj = m[j];
+  // rows written per column: all ld, or (sparse) rows < K plus the padding
+  const int lo = min(K, mj);
+  const int per = sparse ? lo + (ldj - mj) : ldj;
+  const int64_t n = (int64_t)per * (sparse ? rk : K);
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(p / ldj), r = (int)(p % ldj);
-    Q[off[j] + p] = (r < K && c < rk) ? Q1[(int64_t)j * K * K + (int64_t)c * K + r] : 0.0;
+    const int c = (int)(p / per), rr = (int)(p % per);
+    const int r = (sparse && rr >= lo) ? mj + (rr - lo) : rr;
+    Q[off[j] + (int64_t)c * ldj + r] = (r < K && c < rk) ? Q1[(int64_t)j * K * K + (int64_t)c * K + r] : 0.0;
   }
 }
 
@@ -414,7 +421,8 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
     if ((e = fl::wy_apply_nb(a, 32, s))) return e;
   }
   // ---- K2c: Qhat = Q0 [Q1; 0], reflector blocks of Q0 in reverse ----
-  init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, (double*)Q->vals);
+  init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, Q->m, (wide && qf) ? 1 : 0,
+                                                (double*)Q->vals);
   FL_CHECK_LAUNCH();
   if (wide && qf) return fl::qform_fused(fac, A->off, A->ld, A->m, (double*)Q->vals, Q->off, Q->ld, rank, ws.T64, K, J, s);
   const int wb = wide ? 64 : NB;
