@@ -64,6 +64,8 @@ struct PanelArgs {
   int P0;
   double* tau;     // (J, K)
   double* T;       // (J, K/NB, NB, NB) column-major per panel
+  const double* src;  // null, or the store the panel's columns are read from (same layout; the
+                      // first inner panel reads it and writes A, so A needs no prior copy)
 };
 
 template <int W>
@@ -163,12 +165,14 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
   for (int q = 0; q < NB / W; ++q) {
     const int c = P0 + q * W;
     const int Mq = m - c;
+    // columns right of the first inner panel are first read from src, later from A
+    const double* Xj = (q == 0 && a.src) ? a.src + a.off[j] : Aj;
     // load inner panel rows c..m-1 (8-byte cp.async: every load in flight at once)
     for (int k = 0; k < W; ++k)
 #pragma unroll 2
       for (int r = threadIdx.x; r < Mq; r += NT) {
         const unsigned dst = (unsigned)__cvta_generic_to_shared(S + k * Mq + r);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(Aj + (int64_t)(c + k) * ld + c + r)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(Xj + (int64_t)(c + k) * ld + c + r)
                      : "memory");
       }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -185,7 +189,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
       for (int r = threadIdx.x; r < Mq; r += NT) {
         double xv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = Aj[(int64_t)(x0 + u) * ld + c + r];
+        for (int u = 0; u < 4; ++u) xv[u] = Xj[(int64_t)(x0 + u) * ld + c + r];
 #pragma unroll
         for (int k = 0; k < W; ++k) {
           const double v = (r < k) ? 0.0 : ((r == k) ? 1.0 : S[k * Mq + r]);
@@ -213,7 +217,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
           double s = 0.0;
 #pragma unroll
           for (int k = 0; k < W; ++k) s += vv[k] * z[k * 4 + u];
-          Aj[(int64_t)(x0 + u) * ld + c + r] -= s;
+          Aj[(int64_t)(x0 + u) * ld + c + r] = Xj[(int64_t)(x0 + u) * ld + c + r] - s;
         }
       }
       __syncthreads();
@@ -326,13 +330,13 @@ __global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
 
 namespace fl {
 int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t* m, int J, int K, int P0,
-                 double* tau, double* T, cudaStream_t s) {
+                 double* tau, double* T, cudaStream_t s, const double* src) {
   static bool attr = false;
   if (!attr) {
     FL_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
     attr = true;
   }
-  PanelArgs a{A, off, ld, m, K, P0, tau, T};
+  PanelArgs a{A, off, ld, m, K, P0, tau, T, src};
   panel_kernel<<<J, NT, SMEM_S, s>>>(a);
   FL_CHECK_LAUNCH();
   return FL_OK;

@@ -17,7 +17,7 @@
 
 namespace fl {
 int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t* m, int J, int K, int P0,
-                 double* tau, double* T, cudaStream_t s);
+                 double* tau, double* T, cudaStream_t s, const double* src = nullptr);
 int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
             int32_t* rank, double* diag, cudaStream_t s);
 bool qrcp2_ok(int K);
@@ -250,6 +250,15 @@ __global__ void __launch_bounds__(NT) combine_t_kernel(const double* __restrict_
   }
 }
 
+// rows m_j..ld_j-1 of every column of block j set to zero
+__global__ void zero_pad_kernel(double* __restrict__ W, const int64_t* __restrict__ off,
+                                const int32_t* __restrict__ ld, const int32_t* __restrict__ m, int K) {
+  const int j = blockIdx.x;
+  const int ldj = ld[j], mj = m[j], pad = ldj - mj;
+  if (pad <= 0) return;
+  for (int p = threadIdx.x; p < K * pad; p += blockDim.x) W[off[j] + (int64_t)(p / pad) * ldj + mj + p % pad] = 0.0;
+}
+
 // zero tau past the rank (reflectors that were never generated)
 __global__ void clamp_tau_kernel(double* tau, int K, const int32_t* rank) {
   const int j = blockIdx.x;
@@ -331,12 +340,19 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
   double* fac = ws.fac;
 
   // ---- K2a: unpivoted blocked Householder QR ----
+  // the factor copy is written by the first panel step (rows < m_j); its
+  // padding rows m_j..ld_j-1, which the WY kernels stream, are zeroed here
+  zero_pad_kernel<<<J, 256, 0, s>>>(fac, A->off, A->ld, A->m, K);
+  FL_CHECK_LAUNCH();
   int e;
   if (wide) {
     for (int q = 0; q < K / 64; ++q) {
       const int P0 = 64 * q;
-      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s))) return e;
+      // q = 0 reads the raw blocks and writes the factor copy (no separate copy)
+      const double* src = q == 0 ? (const double*)A->vals : nullptr;
+      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s, src))) return e;
       fl::WyArgs a = self_args(A, fac, J, P0, P0 + NB, NB, ws.T0 + (int64_t)(2 * q) * NB * NB, t32s, 1);
+      a.Csrc = src;
       if ((e = fl::wy_apply_nb(a, 32, s))) return e;
       if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0 + NB, ws.tau0, ws.T0, s))) return e;
       combine_t_kernel<<<dim3(1, J), NT, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.T0, ws.T64, q);
@@ -344,16 +360,19 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
       const int ntrail = K - P0 - 64;
       if (ntrail > 0) {
         a = self_args(A, fac, J, P0, P0 + 64, ntrail, ws.T64 + (int64_t)q * 64 * 64, t64s, 1);
+        a.Csrc = src;
         if ((e = fl::wy_apply_nb(a, 64, s))) return e;
       }
     }
   } else {
     for (int p = 0; p < npan; ++p) {
       const int P0 = p * NB;
-      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s))) return e;
+      const double* src = p == 0 ? (const double*)A->vals : nullptr;
+      if ((e = fl::panel_factor(fac, A->off, A->ld, A->m, J, K, P0, ws.tau0, ws.T0, s, src))) return e;
       const int ntrail = K - P0 - NB;
       if (ntrail > 0) {
         fl::WyArgs a = self_args(A, fac, J, P0, P0 + NB, ntrail, ws.T0 + (int64_t)p * NB * NB, t32s, 1);
+        a.Csrc = src;
         if ((e = fl::wy_apply_nb(a, 32, s))) return e;
       }
     }
@@ -480,8 +499,8 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
   if (A->max_rows > 11776 || K > 640) return FL_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   Workspace ws = carve(workspace, J, K, store_elems, nullptr);
-  // the raw blocks stay intact: factor a copy (same layout, absolute offsets)
-  FL_CUDA(cudaMemcpyAsync(ws.fac, A->vals, (size_t)store_elems * 8, cudaMemcpyDeviceToDevice, s));
+  // the raw blocks stay intact: the first K2a step reads them and writes the
+  // factor copy (same layout, absolute offsets)
   const int G = group_count(J);
   if (G == 1) return run_group(A, Q, K, sigma, R, perm, rank, diag, ws, J, s, nullptr);
 

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
   const int vld = a.vld ? a.vld[j] : a.vld_const, cld = a.cld ? a.cld[j] : a.cld_const;
   const double* V = a.V + (a.voff ? a.voff[j] : j * a.vstride) + a.v_col0 * (int64_t)vld;
   double* C = a.C + (a.coff ? a.coff[j] : j * a.cstride) + (a.c_col0 + c0) * (int64_t)cld;
+  const double* Cin = a.Csrc ? a.Csrc + (C - a.C) : C;  // where C is read from
   const int nchunks = (mj - r0 + RC - 1) / RC;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
   __syncthreads();
   auto load = [&](int ch, int G) {
     const int st = G % STAGES;
-    load_chunk<NB>(V, vld, C, cld, ncol, r0 + ch * RC, stage_v(st), stage_c(st));
+    load_chunk<NB>(V, vld, Cin, cld, ncol, r0 + ch * RC, stage_v(st), stage_c(st));
     fl::cp_async_arrive(&full[st]);
   };
   // chunk G's data: wait, then the unit-trapezoid mask on the first chunks

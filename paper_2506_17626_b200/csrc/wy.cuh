@@ -39,6 +39,7 @@ struct WyArgs {
   const int32_t* tiles;   // (ntiles, 2): block, first column (relative to c_col0); nullptr:
   int32_t tiles_per_block;//   block = blockIdx / tiles_per_block, column tile = remainder
   int32_t ntiles;
+  const double* Csrc;     // null, or the store C is read from (same layout; written to C)
 };
 
 int wy_apply(const WyArgs& a, cudaStream_t s);               // NB = 32
