@@ -1,7 +1,7 @@
 // K2b — truncated column-pivoted QR of the triangular factor R0_j of every
 // block (route R: QRCP(A_j) and QRCP(R0_j) choose the same pivots in exact
 // arithmetic because partial column norms are invariant under the
-// orthogonal Q0_j). One CTA per block (256 threads, two CTAs
+// orthogonal Q0_j). One CTA per block (384 threads, one CTA
 // per SM), R0_j (K x K, column-major, ld K) streamed from HBM/L2.
 //
 // Pivot rule and norm bookkeeping follow LAPACK's blocked dlaqps (what
@@ -26,7 +26,13 @@
 
 namespace {
 
-constexpr int NT = 256;
+#ifndef QRCP_NT
+// measured on cfg4 (ncu, one filter): 256 threads x 2 CTAs/SM 89.0 ms;
+// one CTA/SM: 384 threads 80.8 ms (166 registers), 512 81.6, 448 106.7,
+// 320 129.6, 640 117.3; 512 with a 32-column panel 92.3 (spills)
+#define QRCP_NT 384
+#endif
+constexpr int NT = QRCP_NT;
 constexpr int NW = NT / 32;
 #ifndef QRCP_PB
 #define QRCP_PB 16
@@ -47,7 +53,7 @@ constexpr int NW = NT / 32;
 #define QRCP_PREFETCH 0
 #endif
 #ifndef QRCP_MB
-#define QRCP_MB 2
+#define QRCP_MB 1
 #endif
 constexpr int PB = QRCP_PB;  // panel width (F has PB columns)
 
@@ -499,7 +505,7 @@ namespace fl {
 int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
             int32_t* rank, double* diag, cudaStream_t s) {
   const size_t smem = (size_t)(PB * K + 4 * K) * sizeof(double) + (size_t)2 * K * sizeof(int);
-  if (smem > 110 * 1024) return FL_ERR_INVALID;
+  if (smem > (QRCP_MB > 1 ? 110 : 220) * 1024) return FL_ERR_INVALID;
   FL_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   QrcpArgs a{R0, K, kmax, sigma, tau, perm, rank, diag, J};
   int grid = J;
