@@ -14,11 +14,16 @@
 namespace {
 
 constexpr int NB = 32;
-constexpr int NT = 512;
+#ifndef PANEL_NT
+// measured on cfg4: 512 threads 2.11 ms per launch, 384 threads (160
+// registers) 2.34 ms
+#define PANEL_NT 512
+#endif
+constexpr int NT = PANEL_NT;
 constexpr int NW = NT / 32;
 constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
 // (measured: 256 threads at two CTAs per SM, 84 KB panels, was slower: 2.80 vs 2.25 ms per launch)
-constexpr int GC = 64;              // Gram pass row chunk
+constexpr int GC = (NB * 64) % NT == 0 ? 64 : 48;  // Gram pass row chunk (NB * GC divisible by NT)
 constexpr int GLD = GC + 4;
 
 // Sum N (a power of two <= 32) per-thread partials across the CTA; results
