@@ -254,11 +254,12 @@ def test_qr_edge_cases(fl):
     assert fl.qr_column_pivot(dup, 1e-8).kept.size == 5
 
 
-@pytest.mark.parametrize("K", [256, 704])
+@pytest.mark.parametrize("K", [160, 192, 256, 704])
 def test_qr_column_pivot_both_routes_match_scipy(fl, K):
-    """K = 256 takes route R (blocked), K = 704 exceeds its shared-memory
-    bound and takes the direct kernel: both reproduce LAPACK's kept sequence
-    on a gapped-spectrum matrix (linalg.py:58-97)."""
+    """K = 160 / 192 / 256 take route R (blocked: 32-wide updates for K = 160,
+    64-wide and the fused K2c for 192 / 256), K = 704 exceeds its
+    shared-memory bound and takes the direct kernel: all reproduce LAPACK's
+    kept sequence on a gapped-spectrum matrix (linalg.py:58-97)."""
     rng = np.random.default_rng(K)
     m = 900
     u, _ = np.linalg.qr(rng.standard_normal((m, K)))
