@@ -185,47 +185,76 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
     factor_inner<W>(S, Mq, red, sc, Tw, tau_j, c);
     for (int k = 0; k < W; ++k)
       for (int r = threadIdx.x; r < Mq; r += NT) Aj[(int64_t)(c + k) * ld + c + r] = S[k * Mq + r];
-    // apply (I - V Tw V^T)^T to the panel columns right of this inner panel, 4 at a time
-    for (int x0 = c + W; x0 < P0 + NB; x0 += 4) {
-      double p[4 * W];
-#pragma unroll
-      for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
-#pragma unroll 2
-      for (int r = threadIdx.x; r < Mq; r += NT) {
-        double xv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = Xj[(int64_t)(x0 + u) * ld + c + r];
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const double v = (r < k) ? 0.0 : ((r == k) ? 1.0 : S[k * Mq + r]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) p[k * 4 + u] += v * xv[u];
-        }
-      }
-      block_sums<4 * W>(p, red, sc);
-      // z = Tw^T w  (W x 4)
-      __shared__ double z[4 * 8];
-      if (threadIdx.x < 4 * W) {
-        const int k = threadIdx.x / 4, u = threadIdx.x % 4;
-        double s = 0.0;
-        for (int b = 0; b <= k; ++b) s += Tw[k * W + b] * sc[b * 4 + u];  // Tw^T[k][b] = Tw[b][k]
-        z[k * 4 + u] = s;
-      }
-      __syncthreads();
-#pragma unroll 2
-      for (int r = threadIdx.x; r < Mq; r += NT) {
-        double vv[W];
+    // apply (I - V Tw V^T)^T to the panel columns right of this inner panel,
+    // 4 at a time: one pass per group updates group g (with z(g) = Tw^T
+    // V^T x(g)) and forms the dots V^T x(g+1) of the next group from the same
+    // rows (thread r mod NT throughout), so the groups cost one pass and one
+    // reduction each instead of two passes
+    {
+      const int ng = (P0 + NB - (c + W)) / 4;
+      __shared__ double z[2][4 * 8];
+      auto vvals = [&](int r, double (&vv)[W]) {
 #pragma unroll
         for (int k = 0; k < W; ++k) vv[k] = (r < k) ? 0.0 : ((r == k) ? 1.0 : S[k * Mq + r]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < W; ++k) s += vv[k] * z[k * 4 + u];
-          Aj[(int64_t)(x0 + u) * ld + c + r] = Xj[(int64_t)(x0 + u) * ld + c + r] - s;
+      };
+      auto finish = [&](double (&p)[4 * W], int buf) {  // z(buf) = Tw^T (V^T x)
+        block_sums<4 * W>(p, red, sc);
+        if (threadIdx.x < 4 * W) {
+          const int k = threadIdx.x / 4, u = threadIdx.x % 4;
+          double s2 = 0.0;
+          for (int b = 0; b <= k; ++b) s2 += Tw[k * W + b] * sc[b * 4 + u];  // Tw^T[k][b] = Tw[b][k]
+          z[buf][k * 4 + u] = s2;
         }
+        __syncthreads();
+      };
+      if (ng > 0) {
+        double p[4 * W];
+#pragma unroll
+        for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
+        const int x0 = c + W;
+#pragma unroll 2
+        for (int r = threadIdx.x; r < Mq; r += NT) {
+          double vv[W], xv[4];
+          vvals(r, vv);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xv[u] = Xj[(int64_t)(x0 + u) * ld + c + r];
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p[k * 4 + u] += vv[k] * xv[u];
+        }
+        finish(p, 0);
       }
-      __syncthreads();
+      for (int gi = 0; gi < ng; ++gi) {
+        const int x0 = c + W + 4 * gi;
+        const bool nxt = gi + 1 < ng;
+        const volatile double* zg = z[gi & 1];  // re-read per row (hoisted it would pin 4W registers)
+        double p[4 * W];
+#pragma unroll
+        for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
+#pragma unroll 1
+        for (int r = threadIdx.x; r < Mq; r += NT) {
+          double vv[W], xn[4];
+          vvals(r, vv);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xn[u] = nxt ? Xj[(int64_t)(x0 + 4 + u) * ld + c + r] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            double s2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) s2 += vv[k] * zg[k * 4 + u];
+            Aj[(int64_t)(x0 + u) * ld + c + r] = Xj[(int64_t)(x0 + u) * ld + c + r] - s2;
+          }
+          if (nxt) {
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) p[k * 4 + u] += vv[k] * xn[u];
+          }
+        }
+        if (nxt) finish(p, (gi + 1) & 1);
+        else __syncthreads();
+      }
     }
   }
   // ---- T for the 32-column panel from G = V^T V (DMMA over staged chunks) ----
