@@ -16,6 +16,9 @@ namespace {
 
 constexpr int TN = 64;            // C columns per CTA
 constexpr int RC = 32;            // rows per staged chunk
+#ifndef WY_T_SMEM
+#define WY_T_SMEM 0  // 1: T_j staged in shared memory. Measured on cfg4 (wy<64>, 2 filters): staged 79.8 ms, read through L1/L2 75.3 (the 32 KB go to L1)
+#endif
 #ifndef WY_STAGES64
 #define WY_STAGES64 4  // measured on cfg4: 1.4% faster than 3 (296.9 vs 301.1 ms per two filters)
 #endif
@@ -29,7 +32,7 @@ struct Cfg {
   static constexpr int NW = 8 * NB / 32;
   static constexpr int NT = NW * 32;
   static constexpr int STAGES = stages_for<NB>();
-  static constexpr size_t smem = (size_t)(STAGES * NB * LDS + STAGES * TN * LDS + NB * LDW + NB * NB) * 8;
+  static constexpr size_t smem = (size_t)(STAGES * NB * LDS + STAGES * TN * LDS + NB * LDW + (WY_T_SMEM ? NB * NB : 0)) * 8;
 };
 
 template <int NB>
@@ -89,7 +92,12 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
   const int nchunks = (mj - r0 + RC - 1) / RC;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
+#if WY_T_SMEM
   for (int i = threadIdx.x; i < NB * NB; i += Cfg<NB>::NT) Ts[i] = a.T[(int64_t)j * a.tstride + i];
+#else
+  const double* Tg = a.T + (int64_t)j * a.tstride;  // read through L1/L2 in phase 2
+  (void)Ts;
+#endif
 
   auto stage_v = [&](int s) { return Vs + s * NB * LDS; };
   auto stage_c = [&](int s) { return Cs + s * TN * LDS; };
@@ -203,7 +211,11 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
 #pragma unroll
     for (int k0 = 0; k0 < NB; k0 += 4) {
       const int ar = mt * 8 + g, ac = k0 + t;
+#if WY_T_SMEM
       const double av = a.transT ? Ts[ar * NB + ac] : Ts[ac * NB + ar];  // op(T)[ar][ac]
+#else
+      const double av = __ldg(a.transT ? Tg + ar * NB + ac : Tg + ac * NB + ar);
+#endif
 #pragma unroll
       for (int n = 0; n < 4; ++n) fl::dmma(p2[n][0], p2[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
     }
