@@ -51,16 +51,9 @@ constexpr int TN = 64;    // C columns per CTA
 #endif
 constexpr int NW = QF_NW, NT = NW * 32;
 constexpr int RC = 2 * NW;  // rows per staged chunk
-#ifndef QF_SWZ
-#define QF_SWZ 0  // measured on cfg4: swizzled 87.4 vs padded 78.2 ms
-#endif
-// staged tiles: column-major, LDS doubles per column (padded: 4 mod 16 keeps
-// the 8-byte fragment loads conflict-free). QF_SWZ: unpadded columns with the
-// row index XOR 4 (col mod 4) instead (11% less shared memory; slower)
-constexpr int LDS = QF_SWZ ? RC : RC + 4;
-__device__ __forceinline__ int SX(int col, int row) {
-  return QF_SWZ ? col * LDS + (row ^ ((col & 3) << 2)) : col * LDS + row;
-}
+constexpr int LDS = RC + 4; // = 4 mod 16: conflict-free 8-byte fragment loads
+// (measured: an unpadded layout with the row index XOR 4 (col mod 4) —
+// conflict-free as well, 11% less shared memory — 87.4 vs 78.2 ms on cfg4)
 constexpr int LDW = TN + 4;
 constexpr int MT = RC / 8;            // m-tiles per chunk
 constexpr int BNN = 64 / NW / 2;     // phase-B warp tile: 2 m-tiles x BNN n-tiles
@@ -168,16 +161,16 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
       for (int it = 0; it < SLOTS; ++it) {
         const int col = scol[it], rr = srr[it], row = rbase + rr;
         if (doB) {
-          double* d = vs + SX(col, rr);
+          double* d = vs + col * LDS + rr;
           if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bB + col) * vld + row);
           else fl::cp_async16_zero(d, V);
         }
         if (doA) {
-          double* d = vs + NB * LDS + SX(col, rr);
+          double* d = vs + (NB + col) * LDS + rr;
           if (row < vld) fl::cp_async16(d, V + (int64_t)(NB * bA + col) * vld + row);
           else fl::cp_async16_zero(d, V);
         }
-        double* d = cs + SX(col, rr);
+        double* d = cs + col * LDS + rr;
         if (col < ncol && row < cz && row < cld) fl::cp_async16(d, C + (int64_t)col * cld + row);
         else fl::cp_async16_zero(d, C);
       }
@@ -214,11 +207,11 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
             const int col = p / RC, rr = p % RC;
             if (mB) {
               const int rel = rbase + rr - NB * bB;
-              if (rel <= col) vs[SX(col, rr)] = (rel == col) ? 1.0 : 0.0;
+              if (rel <= col) vs[col * LDS + rr] = (rel == col) ? 1.0 : 0.0;
             }
             if (mA) {
               const int rel = rbase + rr - NB * bA;
-              if (rel <= col) vs[NB * LDS + SX(col, rr)] = (rel == col) ? 1.0 : 0.0;
+              if (rel <= col) vs[(NB + col) * LDS + rr] = (rel == col) ? 1.0 : 0.0;
             }
           }
           __syncthreads();
@@ -230,20 +223,20 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
 #pragma unroll
           for (int n = 0; n < 2; ++n) {
             const int col = (an + n) * 8 + 2 * t;
-            c[n][0] = cs[SX(col, row)];
-            c[n][1] = cs[SX(col + 1, row)];
+            c[n][0] = cs[col * LDS + row];
+            c[n][1] = cs[(col + 1) * LDS + row];
           }
 #pragma unroll
           for (int k = 0; k < NB / 4; ++k) {
-            const double av = -vb[SX(4 * k + t, row)];
+            const double av = -vb[(4 * k + t) * LDS + row];
 #pragma unroll
             for (int n = 0; n < 2; ++n) fl::dmma(c[n][0], c[n][1], av, bw[k][n]);
           }
 #pragma unroll
           for (int n = 0; n < 2; ++n) {
             const int col = (an + n) * 8 + 2 * t;
-            cs[SX(col, row)] = c[n][0];
-            cs[SX(col + 1, row)] = c[n][1];
+            cs[col * LDS + row] = c[n][0];
+            cs[(col + 1) * LDS + row] = c[n][1];
             if (rbase + row < mj) {
               if (col < ncol) C[(int64_t)col * cld + rbase + row] = c[n][0];
               if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + rbase + row] = c[n][1];
@@ -264,9 +257,9 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
             const int k0 = 4 * s;
             double av[2], bv[BNN];
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi) av[mi] = vs[SX((bm + mi) * 8 + g, k0 + t)];
+            for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((bm + mi) * 8 + g) * LDS + k0 + t];
 #pragma unroll
-            for (int n = 0; n < BNN; ++n) bv[n] = cs[SX((bn + n) * 8 + g, k0 + t)];
+            for (int n = 0; n < BNN; ++n) bv[n] = cs[((bn + n) * 8 + g) * LDS + k0 + t];
 #pragma unroll
             for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -292,11 +285,11 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
           const int col = p / RC, rr = p % RC;
           if (mB) {
             const int rel = rbase + rr - NB * bB;
-            if (rel <= col) vs[SX(col, rr)] = (rel == col) ? 1.0 : 0.0;
+            if (rel <= col) vs[col * LDS + rr] = (rel == col) ? 1.0 : 0.0;
           }
           if (mA) {
             const int rel = rbase + rr - NB * bA;
-            if (rel <= col) vs[NB * LDS + SX(col, rr)] = (rel == col) ? 1.0 : 0.0;
+            if (rel <= col) vs[(NB + col) * LDS + rr] = (rel == col) ? 1.0 : 0.0;
           }
         }
         __syncthreads();
@@ -309,20 +302,20 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
           const int col = (an + n) * 8 + 2 * t;
-          c[n][0] = cs[SX(col, row)];
-          c[n][1] = cs[SX(col + 1, row)];
+          c[n][0] = cs[col * LDS + row];
+          c[n][1] = cs[(col + 1) * LDS + row];
         }
 #pragma unroll
         for (int k = 0; k < NB / 4; ++k) {
-          const double av = -vb[SX(4 * k + t, row)];
+          const double av = -vb[(4 * k + t) * LDS + row];
 #pragma unroll
           for (int n = 0; n < 2; ++n) fl::dmma(c[n][0], c[n][1], av, bw[k][n]);
         }
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
           const int col = (an + n) * 8 + 2 * t;
-          cs[SX(col, row)] = c[n][0];
-          cs[SX(col + 1, row)] = c[n][1];
+          cs[col * LDS + row] = c[n][0];
+          cs[(col + 1) * LDS + row] = c[n][1];
           if (rbase + row < mj) {
             if (col < ncol) C[(int64_t)col * cld + rbase + row] = c[n][0];
             if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + rbase + row] = c[n][1];
@@ -339,9 +332,9 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
           const int k0 = 4 * s;
           double av[2], bv[BNN];
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi) av[mi] = vs[SX((bm + mi) * 8 + g, k0 + t)];
+          for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((bm + mi) * 8 + g) * LDS + k0 + t];
 #pragma unroll
-          for (int n = 0; n < BNN; ++n) bv[n] = cs[SX((bn + n) * 8 + g, k0 + t)];
+          for (int n = 0; n < BNN; ++n) bv[n] = cs[((bn + n) * 8 + g) * LDS + k0 + t];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
