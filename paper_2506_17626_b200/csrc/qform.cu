@@ -51,7 +51,12 @@ constexpr int TN = 64;    // C columns per CTA
 #endif
 constexpr int NW = QF_NW, NT = NW * 32;
 constexpr int RC = 2 * NW;  // rows per staged chunk
-constexpr int LDS = RC + 4; // = 4 mod 16: conflict-free 8-byte fragment loads
+#ifndef QF_PAD
+#define QF_PAD 4
+#endif
+constexpr int LDS = RC + QF_PAD; // 4: = 4 mod 16, conflict-free 8-byte fragment loads
+// (measured on cfg4: pad 4 78.2 ms, pad 2 — 2-way conflicts, ring small enough
+// for the 164 KB shared-memory configuration — 80.4, pad 0 128 ms)
 // (measured: an unpadded layout with the row index XOR 4 (col mod 4) —
 // conflict-free as well, 11% less shared memory — 87.4 vs 78.2 ms on cfg4)
 constexpr int LDW = TN + 4;
