@@ -196,6 +196,9 @@ typedef struct fl_lsqr_vecs {
   double* x;                /* (n,) */
   double* xbest;            /* (n,) monitor best iterate */
   double* trace;            /* (max_iters+1,) phibar per iteration */
+  double* ub;               /* (partial_len,) or null: u at every block row (block-local
+                               order), kept by the row kernel so the fused kernel reads
+                               its rows contiguously instead of gathering through rows */
 } fl_lsqr_vecs;
 
 /* rhs -> u, beta, v = Q^T u / alpha, w = v (solvers.py:98-117) */

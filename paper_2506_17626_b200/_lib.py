@@ -67,7 +67,7 @@ class LsqrState(C.Structure):
 
 
 class LsqrVecs(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("u", "v", "vp", "w", "x", "xbest", "trace")]
+    _fields_ = [(n, C.c_void_p) for n in ("u", "v", "vp", "w", "x", "xbest", "trace", "ub")]
 
 
 class CgVecs(C.Structure):

@@ -187,8 +187,14 @@ __global__ void __launch_bounds__(NT, MB)
 #pragma unroll
     for (int i = 0; i < RP; ++i) {
       const int r = 2 * (threadIdx.x + i * NT);
-      uh_r[i].x = (r < m) ? vec.u[rows[r]] / beta : 0.0;
-      uh_r[i].y = (r + 1 < m) ? vec.u[rows[r + 1]] / beta : 0.0;
+      if (vec.ub) {  // block-local copy: contiguous
+        const double* ubj = vec.ub + op.row_off[j];
+        uh_r[i].x = (r < m) ? ubj[r] / beta : 0.0;
+        uh_r[i].y = (r + 1 < m) ? ubj[r + 1] / beta : 0.0;
+      } else {
+        uh_r[i].x = (r < m) ? vec.u[rows[r]] / beta : 0.0;
+        uh_r[i].y = (r + 1 < m) ? vec.u[rows[r + 1]] / beta : 0.0;
+      }
       pp_r[i] = make_double2(0.0, 0.0);
     }
     // v_j[tile] is read one tile ahead (broadcast loads, off the critical path)
@@ -451,6 +457,8 @@ __global__ void __launch_bounds__(256) row_kernel(fl_blockop op, fl_lsqr_vecs ve
     }
     const double un = acc / alpha - alpha * (ug / bprev);
     vec.u[g] = un;
+    if (vec.ub)
+      for (int e = e0; e < e1; ++e) vec.ub[op.gsrc[e]] = un;
     ss += un * un;
     g = gn;
     e0 = n0;

@@ -326,6 +326,8 @@ __global__ void __launch_bounds__(NT) lsqr_init_a(fl_blockop op, const double* _
   if (g < op.nrows) {
     const double h = rhs[g];
     vec.u[g] = h;
+    if (vec.ub)
+      for (int e = op.gptr[g]; e < op.gptr[g + 1]; ++e) vec.ub[op.gsrc[e]] = h;
     ss = h * h;
   }
   ss = fl::block_sum(ss, sh);

@@ -156,9 +156,11 @@ class DeviceLsqr:
         self.u = t.empty(max(n_rows, 1), **f64)
         self.v, self.vp, self.w, self.x, self.xbest = (t.zeros(n, **f64) for _ in range(5))
         self.trace = t.zeros(self.max_iters + 2, **f64)
+        # u at every block row (block-local order), for the fused kernel's contiguous reads
+        self.ub = t.empty(max(blocks.layout.partial_len, 1), **f64)
         self.state = t.zeros(C.sizeof(_lib.LsqrState), dtype=t.uint8, device=dev)
         self.vecs = _lib.LsqrVecs(*(D.ptr(a) for a in (self.u, self.v, self.vp, self.w, self.x,
-                                                          self.xbest, self.trace)))
+                                                          self.xbest, self.trace, self.ub)))
 
     def reset_state(self, stride: int, track_best: bool, atol=None, btol=None, conlim=1e8,
                     monitor: bool = False):
