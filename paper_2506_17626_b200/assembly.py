@@ -15,6 +15,7 @@ dirty and the device copy is refreshed before the next device use.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -286,12 +287,11 @@ class AssemblyPlan:
         if len(problem.constraints) > 7:
             raise NotImplementedError("more than 7 constraint groups")
 
-        row_count, box, con_ptr, con_idx, con_grp, rows_per_block = _layout_inputs(
-            problem, dec, basis, axes, counts)
+        K = basis.feature_count
+        row_count, box, con_ptr, con_idx, con_grp, rows_per_block, self.layout = _cached_layout(
+            problem, dec, axes, counts, K, con_pts)
         goff = np.cumsum([0] + [p.shape[0] for p in con_pts])
         con_idx = con_idx + goff[con_grp].astype(np.int32) if con_idx.size else con_idx
-        K = basis.feature_count
-        self.layout = D.BlockLayout(row_count, K, rows_per_block)
         self.rows_per_block = rows_per_block
         self.problem, self.dec, self.basis = problem, dec, basis
         self.axes, self.n_interior, self.row_count = axes, n_interior, row_count
@@ -320,6 +320,37 @@ class AssemblyPlan:
         return GlobalSystem(self.problem, self.dec, self.basis, self.rhs, self.n_interior,
                             self.row_count, self.basis.column_count, self.axes, store=store,
                             block_rows=[r.astype(int) for r in self.rows_per_block])
+
+
+# Row structure of the last few lattices (block runs, constraint membership,
+# global row ids, BlockLayout with its device tables). It depends only on the
+# decomposition's centres and half widths, the lattice axes and the
+# constraint points, so it is keyed by a digest of exactly those arrays: a
+# repeated assemble on the same geometry (e.g. a new basis or right-hand
+# side) skips the host-side layout work; any change of geometry misses.
+_LAYOUT_CACHE: dict = {}
+_LAYOUT_CACHE_MAX = 2
+
+
+def _cached_layout(problem, dec, axes, counts, K, con_pts):
+    h = hashlib.blake2b(digest_size=20)
+    h.update(repr((int(dec.dim), int(dec.count_per_dim), int(K), tuple(int(c) for c in counts),
+                   len(con_pts))).encode())
+    for a in (dec.centers, dec.half_widths, *axes, *con_pts):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        h.update(repr(a.shape).encode())
+        h.update(a.tobytes())
+    key = h.digest()
+    hit = _LAYOUT_CACHE.get(key)
+    if hit is None:
+        row_count, box, con_ptr, con_idx, con_grp, rows_per_block = _layout_inputs(
+            problem, dec, None, axes, counts)
+        hit = (row_count, box, con_ptr, con_idx, con_grp, rows_per_block,
+               D.BlockLayout(row_count, K, rows_per_block))
+        while len(_LAYOUT_CACHE) >= _LAYOUT_CACHE_MAX:
+            _LAYOUT_CACHE.pop(next(iter(_LAYOUT_CACHE)))
+        _LAYOUT_CACHE[key] = hit
+    return hit
 
 
 def _validate(problem, dec, basis):
