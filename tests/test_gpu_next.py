@@ -183,3 +183,29 @@ def test_activations_assembly_matches_reference(fl, name, golden_dir):
                                atol=1e-14 * np.abs(g[name + "_rhs"]).max())
     vals = np.concatenate([b.matrix.ravel() for b in sysd.blocks])
     assert np.abs(vals - g[name + "_vals"]).max() <= 1e-13 * np.abs(g[name + "_vals"]).max()
+
+
+def test_assembly_layout_cache_keyed_by_geometry():
+    """The cached lattice row structure is reused only for identical geometry:
+    a decomposition with another overlap gets its own rows (and the assembled
+    system matches a fresh, uncached assembly)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_17626_b200 as fl
+    from paper_2506_17626_b200 import assembly as A, workloads
+    from paper_2506_17626_b200.domains import decompose
+    wl = workloads.build("cfg1")
+    s1 = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    s2 = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    assert [r.tolist() for r in s1.block_rows] == [r.tolist() for r in s2.block_rows]
+    A._LAYOUT_CACHE.clear()
+    s3 = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    assert [r.tolist() for r in s1.block_rows] == [r.tolist() for r in s3.block_rows]
+    np.testing.assert_array_equal(s1.rhs, s3.rhs)
+    # another overlap: different supports, so different rows
+    dec2 = decompose(wl.dec.domain, wl.dec.count_per_dim, wl.dec.overlap_ratio * 1.3)
+    k1 = A._cached_layout(wl.problem, wl.dec, s1.lattice_axes, [a.size for a in s1.lattice_axes], 64, [])
+    k2 = A._cached_layout(wl.problem, dec2, s1.lattice_axes, [a.size for a in s1.lattice_axes], 64, [])
+    assert k1[-1] is not k2[-1]
+    assert sum(r.size for r in k2[5]) > sum(r.size for r in k1[5])
