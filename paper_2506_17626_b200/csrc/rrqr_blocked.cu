@@ -416,7 +416,9 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
                              rank)))
       return e;
   } else
-  // panels in reverse, columns >= P0 only
+  // panels in reverse, columns >= P0 only (measured: 64-wide blocks with
+  // combined T's, 9.95 ms per filter incl. the combine, vs 8.3 for these
+  // 32-wide launches on the 512-row factors)
   for (int p = npan - 1; p >= 0; --p) {
     const int P0 = p * NB;
     fl::WyArgs a{};
