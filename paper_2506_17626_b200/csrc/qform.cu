@@ -40,14 +40,8 @@ constexpr int TN = 64;    // C columns per CTA
 #ifndef QF_MINB
 #define QF_MINB 1
 #endif
-#ifndef QF_LAG
-// 1: accumulate chunk ch-1 while updating chunk ch (per-stage "updated"
-// mbarriers instead of the 4-warp barrier; needs a 4-stage ring). Measured
-// on cfg4: 96.5 vs 78.2 ms (pipe 63% vs 78%): off.
-#define QF_LAG 0
-#endif
 #ifndef QF_STAGES
-#define QF_STAGES (QF_LAG ? 4 : 3)
+#define QF_STAGES 3
 #endif
 constexpr int NW = QF_NW, NT = NW * 32;
 constexpr int RC = 2 * NW;  // rows per staged chunk
@@ -130,12 +124,11 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
   double bw[NB / 4][2];  // W'(4k + t, 8 (an + n) + g)
   double acc[2][BNN][2];
 
-  __shared__ uint64_t full[STAGES], empty[STAGES], upd[STAGES];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       fl::mbar_init(&full[i], NT);   // one cp.async arrival per thread
       fl::mbar_init(&empty[i], NW);  // one arrival per warp
-      fl::mbar_init(&upd[i], NW);    // (lagged form) chunk updated, one arrival per warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -187,95 +180,6 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
     // their phase of parity (G / STAGES) & 1 for it. No CTA barrier per
     // chunk: a warp waits for its chunk's data (full) and, before refilling a
     // stage, for every warp to have left it (empty), which is a chunk later.
-#if QF_LAG
-    // Lagged form: iteration ch updates chunk ch (A) and accumulates chunk
-    // ch-1 (B), which every warp updated in the previous iteration and
-    // published on upd[stage]; no barrier between A and B. A chunk's stage is
-    // released after its B and refilled two chunks later (STAGES >= 4).
-    static_assert(STAGES >= 4, "lagged form needs two chunks of slack");
-    for (int c = 0; c < STAGES - 2 && c < nch; ++c) load(c, (G0 + c) % STAGES);
-    for (int ch = 0; ch <= nch; ++ch) {
-      const int G = G0 + ch, st = G % STAGES;
-      const int rbase = rlo + ch * RC;
-      if (ch + STAGES - 2 < nch) {
-        const int Gn = G + STAGES - 2, sn = Gn % STAGES;
-        if (ch >= 2) fl::mbar_wait(&empty[sn], ((G - 2) / STAGES) & 1);
-        load(ch + STAGES - 2, sn);
-      }
-      if (ch < nch) {
-        fl::mbar_wait(&full[st], (G / STAGES) & 1);
-        double* vs = Vs + st * VST;
-        double* cs = Cs + st * CST;
-        const bool mB = doB && rbase < NB * bB + NB, mA = doA && rbase < NB * bA + NB;
-        if (mB || mA) {
-          for (int p = threadIdx.x; p < NB * RC; p += NT) {
-            const int col = p / RC, rr = p % RC;
-            if (mB) {
-              const int rel = rbase + rr - NB * bB;
-              if (rel <= col) vs[col * LDS + rr] = (rel == col) ? 1.0 : 0.0;
-            }
-            if (mA) {
-              const int rel = rbase + rr - NB * bA;
-              if (rel <= col) vs[(NB + col) * LDS + rr] = (rel == col) ? 1.0 : 0.0;
-            }
-          }
-          __syncthreads();
-        }
-        if (doA && rbase + RC > NB * bA) {
-          const double* vb = vs + NB * LDS;
-          double c[2][2];
-          const int row = am * 8 + g;
-#pragma unroll
-          for (int n = 0; n < 2; ++n) {
-            const int col = (an + n) * 8 + 2 * t;
-            c[n][0] = cs[col * LDS + row];
-            c[n][1] = cs[(col + 1) * LDS + row];
-          }
-#pragma unroll
-          for (int k = 0; k < NB / 4; ++k) {
-            const double av = -vb[(4 * k + t) * LDS + row];
-#pragma unroll
-            for (int n = 0; n < 2; ++n) fl::dmma(c[n][0], c[n][1], av, bw[k][n]);
-          }
-#pragma unroll
-          for (int n = 0; n < 2; ++n) {
-            const int col = (an + n) * 8 + 2 * t;
-            cs[col * LDS + row] = c[n][0];
-            cs[(col + 1) * LDS + row] = c[n][1];
-            if (rbase + row < mj) {
-              if (col < ncol) C[(int64_t)col * cld + rbase + row] = c[n][0];
-              if (col + 1 < ncol) C[(int64_t)(col + 1) * cld + rbase + row] = c[n][1];
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) fl::mbar_arrive(&upd[st]);
-      }
-      if (ch >= 1) {
-        const int Gb = G - 1, sb = Gb % STAGES;
-        if (doB) {
-          fl::mbar_wait(&upd[sb], (Gb / STAGES) & 1);
-          const double* vs = Vs + sb * VST;
-          const double* cs = Cs + sb * CST;
-#pragma unroll
-          for (int s = 0; s < RC / 4; ++s) {
-            const int k0 = 4 * s;
-            double av[2], bv[BNN];
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi) av[mi] = vs[((bm + mi) * 8 + g) * LDS + k0 + t];
-#pragma unroll
-            for (int n = 0; n < BNN; ++n) bv[n] = cs[((bn + n) * 8 + g) * LDS + k0 + t];
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-              for (int n = 0; n < BNN; ++n) fl::dmma(acc[mi][n][0], acc[mi][n][1], av[mi], bv[n]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) fl::mbar_arrive(&empty[sb]);
-      }
-    }
-#else
     for (int c = 0; c < STAGES - 1 && c < nch; ++c) load(c, (G0 + c) % STAGES);
     for (int ch = 0; ch < nch; ++ch) {
       const int G = G0 + ch, st = G % STAGES;
@@ -356,7 +260,6 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
         load(ch + STAGES - 1, sn);
       }
     }
-#endif
     G0 += nch;
     if (!doB) break;
 
