@@ -52,6 +52,14 @@ constexpr int NW = NT / 32;
 // are evicted again before the gemv reaches them at 296 blocks in flight)
 #define QRCP_PREFETCH 0
 #endif
+#ifndef QRCP_L1KEEP
+// F-gemv loads: column groups starting < QRCP_L1KEEP trailing columns past the
+// pivot use L1::evict_last, the rest L1::no_allocate. Measured on cfg4 (one
+// filter): plain loads 80.8 ms; all no_allocate 79.7; keep 32 / 64 / 96 / 128
+// / 160 / 192 / 256: 76.4 / 74.8 / 74.6 / 73.2 / 74.3 / 76.0 / 78.4; all
+// evict_last 81.6
+#define QRCP_L1KEEP 128
+#endif
 #ifndef QRCP_MB
 #define QRCP_MB 1
 #endif
@@ -68,6 +76,17 @@ struct QrcpArgs {
   double* diag;        // (J, K) |R_ii| / |R_00|
   int J;
 };
+
+__device__ __forceinline__ double2 ld_keep(const double* p) {
+  double2 v;
+  asm volatile("ld.global.L1::evict_last.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
 
 __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
 #pragma unroll
@@ -283,11 +302,23 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             const double w0 = two ? wv(r2) : 0.0;
             const double w1 = (r2 + 1 < M) ? wv(r2 + 1) : 0.0;
             double2 x[CU], y[CU];
+#if QRCP_L1KEEP
+            // the first QRCP_L1KEEP trailing columns stay in L1 across the
+            // panel's steps (the gemv re-reads the same panel-start matrix);
+            // the rest stream past L1
+            const bool keep = c0 < QRCP_L1KEEP;
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              x[u] = keep ? ld_keep(cc[u] + r) : ld_stream(cc[u] + r);
+              y[u] = two ? (keep ? ld_keep(cc[u] + r2) : ld_stream(cc[u] + r2)) : make_double2(0.0, 0.0);
+            }
+#else
 #pragma unroll
             for (int u = 0; u < CU; ++u) {
               x[u] = *reinterpret_cast<const double2*>(cc[u] + r);
               y[u] = two ? *reinterpret_cast<const double2*>(cc[u] + r2) : make_double2(0.0, 0.0);
             }
+#endif
 #pragma unroll
             for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
           }
