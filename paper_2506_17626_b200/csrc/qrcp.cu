@@ -88,6 +88,24 @@ __device__ __forceinline__ double2 ld_stream(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ double ld_keep1(const double* p) {
+  double v;
+  asm volatile("ld.global.L1::evict_last.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
+#ifndef QRCP_HINTS2
+#define QRCP_HINTS2 1
+#endif
+#if QRCP_HINTS2
+// panel columns (re-read by the auxv dots every step of the panel) kept in
+// L1; the block update's once-per-panel read-modify-write streams past it
+#define QRCP_LD_PANEL(p) ld_keep1(p)
+#define QRCP_LD_UPD(p) ld_stream(p)
+#else
+#define QRCP_LD_PANEL(p) (*(p))
+#define QRCP_LD_UPD(p) (*reinterpret_cast<const double2*>(p))
+#endif
+
 __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -334,7 +352,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           for (int r0 = i + lane; r0 < M; r0 += 32 * 8) {  // 8 loads in flight per lane
             double x[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) x[q] = (r0 + 32 * q < M) ? cc[r0 + 32 * q] : 0.0;
+            for (int q = 0; q < 8; ++q) x[q] = (r0 + 32 * q < M) ? QRCP_LD_PANEL(cc + r0 + 32 * q) : 0.0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               if (r0 + 32 * q < M) dd += x[q] * wv(r0 + 32 * q);
@@ -466,8 +484,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
 #pragma unroll
           for (int t = 0; t < NTL; ++t) {
             const int row = rs + 8 * t + 2 * t4;
-            c[t] = (col < N && row < M) ? *reinterpret_cast<const double2*>(A + (int64_t)col * K + row)
-                                        : make_double2(0.0, 0.0);
+            c[t] = (col < N && row < M) ? QRCP_LD_UPD(A + (int64_t)col * K + row) : make_double2(0.0, 0.0);
           }
         };
         double2 cc[NTL], cn[NTL], cn2[NTL];
