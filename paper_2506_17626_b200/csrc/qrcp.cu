@@ -22,6 +22,8 @@
 #include <float.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "wy.cuh"
 
 namespace {
@@ -312,34 +314,30 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             d[u] = 0.0;
             cc[u] = A + (int64_t)(i + 1 + min(c0 + u, ncol - 1)) * K;
           }
-          for (int r = i0 + 2 * lane; r < M; r += 128) {
-            const int r2 = r + 64;
-            const double v0 = (r >= i) ? wv(r) : 0.0;
-            const double v1 = (r + 1 < M) ? wv(r + 1) : 0.0;
-            const bool two = r2 < M;
-            const double w0 = two ? wv(r2) : 0.0;
-            const double w1 = (r2 + 1 < M) ? wv(r2 + 1) : 0.0;
-            double2 x[CU], y[CU];
-#if QRCP_L1KEEP
-            // the first QRCP_L1KEEP trailing columns stay in L1 across the
-            // panel's steps (the gemv re-reads the same panel-start matrix);
-            // the rest stream past L1
-            const bool keep = c0 < QRCP_L1KEEP;
+          // the first QRCP_L1KEEP trailing columns stay in L1 across the
+          // panel's steps (the gemv re-reads the same panel-start matrix);
+          // the rest stream past L1. One loop per load kind (no select).
+          auto rows_loop = [&](auto keep_tag) {
+            constexpr bool KEEPL1 = decltype(keep_tag)::value;
+            for (int r = i0 + 2 * lane; r < M; r += 128) {
+              const int r2 = r + 64;
+              const double v0 = (r >= i) ? wv(r) : 0.0;
+              const double v1 = (r + 1 < M) ? wv(r + 1) : 0.0;
+              const bool two = r2 < M;
+              const double w0 = two ? wv(r2) : 0.0;
+              const double w1 = (r2 + 1 < M) ? wv(r2 + 1) : 0.0;
+              double2 x[CU], y[CU];
 #pragma unroll
-            for (int u = 0; u < CU; ++u) {
-              x[u] = keep ? ld_keep(cc[u] + r) : ld_stream(cc[u] + r);
-              y[u] = two ? (keep ? ld_keep(cc[u] + r2) : ld_stream(cc[u] + r2)) : make_double2(0.0, 0.0);
+              for (int u = 0; u < CU; ++u) {
+                x[u] = KEEPL1 ? ld_keep(cc[u] + r) : ld_stream(cc[u] + r);
+                y[u] = two ? (KEEPL1 ? ld_keep(cc[u] + r2) : ld_stream(cc[u] + r2)) : make_double2(0.0, 0.0);
+              }
+#pragma unroll
+              for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
             }
-#else
-#pragma unroll
-            for (int u = 0; u < CU; ++u) {
-              x[u] = *reinterpret_cast<const double2*>(cc[u] + r);
-              y[u] = two ? *reinterpret_cast<const double2*>(cc[u] + r2) : make_double2(0.0, 0.0);
-            }
-#endif
-#pragma unroll
-            for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
-          }
+          };
+          if (c0 < QRCP_L1KEEP) rows_loop(std::true_type{});
+          else rows_loop(std::false_type{});
           {
             const double s = fl::warp_multi_sum<CU>(d);  // lane l: column u = l / (32 / CU)
             const int u = lane / (32 / CU);
