@@ -62,6 +62,13 @@ constexpr int NW = NT / 32;
 // evict_last 81.6
 #define QRCP_L1KEEP 128
 #endif
+#ifndef QRCP_PRESCALE
+// 1: the reflector is scaled in shared memory once per step (one barrier)
+// and the gemv / auxv read it as is; 0: scaled on the fly by its readers.
+// Measured on cfg4: on the fly 89.7 vs 91.3 with the two-CTA shape, but with
+// the L1-hinted gemv the readers' scaling dominates: 67.5 vs 72.6 ms
+#define QRCP_PRESCALE 1
+#endif
 #ifndef QRCP_MB
 #define QRCP_MB 1
 #endif
@@ -140,6 +147,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   __shared__ double fred[8 * NW];
   __shared__ double rowi[PB + 1];
   __shared__ int s_stop, s_rank, s_flagged, s_p;
+  __shared__ double s_alpha;
 
   double* A = q.R0 + (int64_t)j * K * K;
   double* tau = q.tau + (int64_t)j * K;
@@ -228,6 +236,9 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             if (kk < k) xp -= pa[kk] * F[kk * K + p];
           v[r - i] = xp;
           if (r > i) ss += xp * xp;
+#if QRCP_PRESCALE
+          if (r == i) s_alpha = xp;
+#endif
         }
       }
       ss = fl::warp_sum(ss);
@@ -268,7 +279,11 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       ss = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) ss += red[w];
+#if QRCP_PRESCALE
+      const double alpha = s_alpha;
+#else
       const double alpha = v[0];
+#endif
       const double xnorm = sqrt(ss);
       double beta, t;
       if (xnorm == 0.0) {
@@ -288,17 +303,31 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         __syncthreads();
         break;
       }
-      // v stays unscaled in shared memory: its readers below form
-      // w_r = v[r-i] * scal (the value dlarfg's dscal stores, bit for bit)
-      // and w_i = 1 themselves, which saves two barriers per step
+      // v = x * scal (dlarfg's dscal), v_i = 1: prescaled in shared memory, or
+      // (QRCP_PRESCALE 0) left unscaled and formed by its readers bit for bit
       const double scal = (xnorm == 0.0) ? 1.0 : 1.0 / (alpha - beta);
+#if QRCP_PRESCALE
+      // scaled reflector in shared memory once (one more barrier), read as is below
+      for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
+        const double x = v[r - i] * scal;
+        v[r - i] = x;
+        ci[r] = x;  // reflector below the diagonal
+      }
+      if (threadIdx.x == 0) v[0] = 1.0;
+      __syncthreads();
+#else
       for (int r = i + 1 + threadIdx.x; r < M; r += NT) ci[r] = v[r - i] * scal;  // reflector below the diagonal
+#endif
       if (threadIdx.x == 0) {
         tau[i] = t;
         ci[i] = beta;
         q.diag[(int64_t)j * K + i] = fabs(beta);
       }
+#if QRCP_PRESCALE
+      auto wv = [&](int r) { return v[r - i]; };
+#else
       auto wv = [&](int r) { return r == i ? 1.0 : v[r - i] * scal; };
+#endif
       // ---- F(i+1:N, k) = t A(i:M, i+1:N)^T v ; auxv = -t A(i:M, offset:i)^T v ----
       {
         const int ncol = N - i - 1;
