@@ -69,6 +69,9 @@ constexpr int NW = NT / 32;
 // the L1-hinted gemv the readers' scaling dominates: 67.5 vs 72.6 ms
 #define QRCP_PRESCALE 1
 #endif
+#ifndef QRCP_DYN
+#define QRCP_DYN 0  // 1: gemv column groups from a shared counter (measured 68.1 vs 67.6 ms)
+#endif
 #ifndef QRCP_MB
 #define QRCP_MB 1
 #endif
@@ -148,6 +151,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   __shared__ double rowi[PB + 1];
   __shared__ int s_stop, s_rank, s_flagged, s_p;
   __shared__ double s_alpha;
+  __shared__ int s_next;
 
   double* A = q.R0 + (int64_t)j * K * K;
   double* tau = q.tau + (int64_t)j * K;
@@ -243,6 +247,9 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
       ss = fl::warp_sum(ss);
       if (lane == 0) red[wid] = ss;
+#if QRCP_DYN
+      if (threadIdx.x == 0) s_next = 0;
+#endif
       __syncthreads();
       // row i of the trailing columns (final once the swap is done) and of
       // the panel columns: 8-byte cp.async into shared memory, waited for
@@ -335,7 +342,19 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         // the even row i0 <= i (row i-1 contributes v = 0); two chunks per trip
         constexpr int CU = QRCP_CU;  // columns in flight per warp
         const int i0 = i & ~1;
+#if QRCP_DYN
+        // column groups handed out by a shared counter (reset before the
+        // step's first barrier): warps that drew L1-resident or shorter
+        // groups take more, so the barrier after the gemv waits less
+        auto next_group = [&]() {
+          int gidx = 0;
+          if (lane == 0) gidx = atomicAdd(&s_next, 1);
+          return __shfl_sync(0xffffffffu, gidx, 0) * CU;
+        };
+        for (int c0 = next_group(); c0 < ncol; c0 = next_group()) {
+#else
         for (int c0 = wid * CU; c0 < ncol; c0 += NW * CU) {
+#endif
           double d[CU];
           const double* cc[CU];
 #pragma unroll
