@@ -21,7 +21,11 @@ constexpr int NB = 32;
 #endif
 constexpr int NT = PANEL_NT;
 constexpr int NW = NT / 32;
-constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
+// (measured on cfg4: 184 KB 2.09 ms per launch, 164 KB 2.14, 132 KB (W = 4) 2.50)
+#ifndef PANEL_SMEM_KB
+#define PANEL_SMEM_KB 184
+#endif
+constexpr int SMEM_S = PANEL_SMEM_KB * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
 // (measured: 256 threads at two CTAs per SM, 84 KB panels, was slower: 2.80 vs 2.25 ms per launch)
 constexpr int GC = (NB * 64) % NT == 0 ? 64 : 48;  // Gram pass row chunk (NB * GC divisible by NT)
 constexpr int GLD = GC + 4;
