@@ -22,8 +22,12 @@ constexpr int RC = 32;            // rows per staged chunk
 #ifndef WY_STAGES64
 #define WY_STAGES64 4  // measured on cfg4: 1.4% faster than 3 (296.9 vs 301.1 ms per two filters)
 #endif
+// (measured on cfg4, wy<32>, 2 filters: 3 stages 30.3 ms, 2 stages 38.8, 4 stages 42.3)
+#ifndef WY_STAGES32
+#define WY_STAGES32 3
+#endif
 template <int NB>
-constexpr int stages_for() { return NB == 64 ? WY_STAGES64 : 3; }
+constexpr int stages_for() { return NB == 64 ? WY_STAGES64 : WY_STAGES32; }
 constexpr int LDS = RC + 4;       // padded column length of a staged chunk
 constexpr int LDW = TN + 4;       // padded row length of W
 
