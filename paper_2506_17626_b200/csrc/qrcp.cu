@@ -17,8 +17,10 @@
 // the kernel is organised for memory-level parallelism: the column swap is
 // fused with the pivot column's panel update (whose k panel values per row
 // are loaded together), the F-gemv keeps eight columns x two 64-row chunks
-// in flight per warp with 16-byte loads, and the auxv dots issue eight loads
-// per lane at a time.
+// in flight per warp with 16-byte loads (the columns nearest the pivot with
+// an L1 evict_last hint, since every step of a panel re-reads the same
+// panel-start matrix), and the auxv dots issue eight loads per lane at a
+// time.
 #include <float.h>
 #include <stdlib.h>
 

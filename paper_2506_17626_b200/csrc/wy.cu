@@ -6,8 +6,8 @@
 // chunk), twice: phase 1 accumulates
 // W = V^T C (NB x TN) with the k (row) dimension split over two warp groups
 // (each warp: 2 x 4 mma tiles, 6 fragment loads per 8 DMMA), phase 2 forms
-// W' = op(T) W, phase 3 updates C -= V W' with W' held in registers and
-// writes each chunk back through shared memory with 16-byte stores.
+// W' = op(T) W (T read through L1/L2), phase 3 updates C -= V W' with W'
+// held in registers and stores the accumulators straight to global memory.
 // NB = 64 doubles the arithmetic intensity per pass over C (4*NB flops per
 // 24 bytes), which moves the update from the HBM roof to the DMMA roof.
 #include "wy.cuh"
