@@ -39,7 +39,7 @@
 #include "common.cuh"
 
 #ifndef ROW_CTAS_PER_SM
-#define ROW_CTAS_PER_SM 4
+#define ROW_CTAS_PER_SM 3
 #endif
 #ifndef FL_Q_EVICT_FIRST
 // 1: Q's TMA loads with an L2 evict_first policy. Measured on cfg4: 1.444 vs
@@ -439,11 +439,14 @@ __global__ void __launch_bounds__(256) row_kernel(fl_blockop op, fl_lsqr_vecs ve
   int g = gtid;
   int e0 = 0, e1 = 0;
   double ug = 0.0;
+  int src[ME];  // the first ME sources of row g, fetched one row ahead
   if (g < op.nrows) {
     e0 = op.gptr[g];
     e1 = op.gptr[g + 1];
     ug = vec.u[g];
   }
+#pragma unroll
+  for (int q = 0; q < ME; ++q) src[q] = (g < op.nrows && e0 + q < e1) ? op.gsrc[e0 + q] : 0;
   while (g < op.nrows) {
     const int gn = g + gsz;
     int n0 = 0, n1 = 0;
@@ -453,33 +456,41 @@ __global__ void __launch_bounds__(256) row_kernel(fl_blockop op, fl_lsqr_vecs ve
       n1 = op.gptr[gn + 1];
       un_next = vec.u[gn];
     }
+    double pv[ME][FL_LSQR_SPLIT_MAX];
+#pragma unroll
+    for (int q = 0; q < ME; ++q)
+#pragma unroll
+      for (int h = 0; h < FL_LSQR_SPLIT_MAX; ++h)
+        pv[q][h] = (e0 + q < e1 && h < S) ? op.partial[h * op.partial_len + src[q]] : 0.0;
+    int srcn[ME];  // next row's sources, in flight with this row's partials
+#pragma unroll
+    for (int q = 0; q < ME; ++q) srcn[q] = (gn < op.nrows && n0 + q < n1) ? op.gsrc[n0 + q] : 0;
     double acc = 0.0;
-    for (int eb = e0; eb < e1; eb += ME) {
-      int64_t src[ME];
 #pragma unroll
-      for (int q = 0; q < ME; ++q) src[q] = (eb + q < e1) ? op.gsrc[eb + q] : 0;
-      double pv[ME][FL_LSQR_SPLIT_MAX];
-#pragma unroll
-      for (int q = 0; q < ME; ++q)
+    for (int q = 0; q < ME; ++q)
+      if (e0 + q < e1)
 #pragma unroll
         for (int h = 0; h < FL_LSQR_SPLIT_MAX; ++h)
-          pv[q][h] = (eb + q < e1 && h < S) ? op.partial[h * op.partial_len + src[q]] : 0.0;
-#pragma unroll
-      for (int q = 0; q < ME; ++q)
-        if (eb + q < e1)
-#pragma unroll
-          for (int h = 0; h < FL_LSQR_SPLIT_MAX; ++h)
-            if (h < S) acc += pv[q][h];
+          if (h < S) acc += pv[q][h];
+    for (int e = e0 + ME; e < e1; ++e) {  // rows with more than ME sources (3-D)
+      const int64_t sx = op.gsrc[e];
+      for (int h = 0; h < S; ++h) acc += op.partial[h * op.partial_len + sx];
     }
     const double un = acc / alpha - alpha * (ug / bprev);
     vec.u[g] = un;
-    if (vec.ub)
-      for (int e = e0; e < e1; ++e) vec.ub[op.gsrc[e]] = un;
+    if (vec.ub) {
+#pragma unroll
+      for (int q = 0; q < ME; ++q)
+        if (e0 + q < e1) vec.ub[src[q]] = un;
+      for (int e = e0 + ME; e < e1; ++e) vec.ub[op.gsrc[e]] = un;
+    }
     ss += un * un;
     g = gn;
     e0 = n0;
     e1 = n1;
     ug = un_next;
+#pragma unroll
+    for (int q = 0; q < ME; ++q) src[q] = srcn[q];
   }
   for (int64_t c = gtid; c < op.ncols_total; c += gsz) {
     const double vv = vec.vp[c] / alpha;  // v = v'/alpha (:141)
@@ -616,7 +627,7 @@ int fused(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t i
 int row_grid(const fl_blockop* op) {
   const int64_t n = op->nrows > op->ncols_total ? op->nrows : op->ncols_total;
   int64_t g = (n + 255) / 256;
-  if (g > 148 * ROW_CTAS_PER_SM) g = 148 * ROW_CTAS_PER_SM;  // one wave (64 registers per thread)
+  if (g > 148 * ROW_CTAS_PER_SM) g = 148 * ROW_CTAS_PER_SM;  // one wave (80 registers per thread)
   return (int)(g < 1 ? 1 : g);
 }
 
