@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           // the panel values are loaded together (one round trip, not k)
           double pa[PB];
 #pragma unroll
-          for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk < k) ? A[(int64_t)(offset + kk) * K + r] : 0.0;
+          for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk < k) ? QRCP_LD_PANEL(A + (int64_t)(offset + kk) * K + r) : 0.0;
 #pragma unroll
           for (int kk = 0; kk < PB; ++kk)
             if (kk < k) xp -= pa[kk] * F[kk * K + p];
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
             double pa[PB];
 #pragma unroll
-            for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk <= k) ? A[(int64_t)(offset + kk) * K + r] : 0.0;
+            for (int kk = 0; kk < PB; ++kk) pa[kk] = (kk <= k) ? QRCP_LD_PANEL(A + (int64_t)(offset + kk) * K + r) : 0.0;
             double x[FB];
 #pragma unroll
             for (int f = 0; f < FB; ++f) x[f] = (f < nb) ? A[(int64_t)flag[f0 + f] * K + r] : 0.0;
