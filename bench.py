@@ -168,7 +168,7 @@ def launches_per_step(fs, iters):
         else:
             k2a = npan + (npan - 1)
             k2c = npan
-        rrqr = k2a + 5 + npan + 1 + k2c      # extract, qrcp, clamp, build_t, init_q1_r, Q1, init_qhat
+        rrqr = 1 + k2a + 5 + npan + 1 + k2c  # zero_pad, K2a, extract, qrcp, clamp, build_t, init_q1_r, Q1, init_qhat, K2c
         # per block group (rrqr_blocked.cu group_count: FEATLSQ_RRQR_GROUPS, default 1,
         # reduced until every group has >= 32 blocks)
         g = max(1, min(int(os.environ.get("FEATLSQ_RRQR_GROUPS", "1")), 8))
