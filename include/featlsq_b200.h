@@ -130,7 +130,7 @@ typedef struct fl_assembly_desc {
                                lattice point = sum_i index_i * stride_i) */
 } fl_assembly_desc;
 
-#define FL_ASM_TILE 64
+#define FL_ASM_TILE 256
 
 int fl_assemble(const fl_assembly_desc* desc, const fl_blockop* out, void* stream);
 
@@ -153,8 +153,14 @@ int fl_rrqr(const fl_blockop* blocks, int32_t K, int32_t max_rows, double sigma,
  * Q_j = Q0 [Q1; 0]. `A` is left unchanged; Q_j is written to the store `Q`
  * (same layout as A). `workspace` needs fl_rrqr_blocked_workspace() bytes;
  * store_elems = total doubles of the A store. No host synchronisation.
- * Shared-memory bounds: K <= 640 and max_rows <= 11776 (else FL_ERR_INVALID;
- * fl_rrqr covers the rest). */
+ * Shared-memory bounds: K <= FL_RRQR_BLOCKED_MAX_K and max_rows <=
+ * FL_RRQR_BLOCKED_MAX_ROWS (else FL_ERR_INVALID). fl_rrqr stages one
+ * max_rows-long reflector on chip: 8 * (4 K + max_rows) + 4 K bytes <= 220 KB
+ * (about 25.8k rows at K = 512), else FL_ERR_INVALID; the host maps blocks
+ * beyond both bounds to CapExceededError. */
+#define FL_RRQR_BLOCKED_MAX_K 640
+#define FL_RRQR_BLOCKED_MAX_ROWS 11776
+#define FL_RRQR_DIRECT_SMEM_MAX (220 * 1024)
 int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t store_elems);
 int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
                     double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,

@@ -2,7 +2,10 @@
 assemble -> filter_system (truncated RRQR) -> precondition -> lsqr ->
 recover_solution, with the same names, signatures and object surface as the
 reference stage API (featlsq assembly.py:124, filtering.py:92/165/169,
-solvers.py:87). Kernels: csrc/*.cu, C-ABI: include/featlsq_b200.h.
+solvers.py:87). Kernels: csrc/*.cu, C-ABI: include/featlsq_b200.h. The
+package plugs into featlsq (`_featlsq.py`): value types, problem builders
+and exceptions are featlsq's own; `integrate.enable()` rebinds featlsq's
+stage functions to this package.
 """
 
 from .assembly import (GlobalSystem, SolutionBlocks, SubdomainBlock, TestSet, apply,
@@ -17,8 +20,16 @@ from .filtering import (FilteredBlock, FilteredSystem, PreconditionedOperator, f
 from .linalg import PivotedQR, RandomSource, back_substitute, lattice_counts, qr_column_pivot
 from .jets import Jet2, radial_jet
 from .monitor import DeviceL1Error, test_error_fn
-from .problems import (ConstraintRows, LinearOperator2, ProblemSpec, laplace_problem,
-                       oscillator_problem, wave_problem)
+from ._featlsq import featlsq
+
+# featlsq's own value types and problem builders (inputs of the stage API;
+# the same objects, re-exported for convenience)
+ConstraintRows = featlsq.ConstraintRows
+LinearOperator2 = featlsq.LinearOperator2
+ProblemSpec = featlsq.ProblemSpec
+laplace_problem = featlsq.laplace_problem
+oscillator_problem = featlsq.oscillator_problem
+wave_problem = featlsq.wave_problem
 from .solvers import (AdditiveSchwarz, ConvergenceMonitor, Operator, SolveResult, as_operator,
                       as_preconditioner, cg_normal, lsqr)
 

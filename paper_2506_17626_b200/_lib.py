@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("FEATLSQ_LIB") or os.path.join(HERE, "libfeatlsq_b200.
 
 FL_OK, FL_ERR_INVALID, FL_ERR_DEGENERATE, FL_ERR_DIVERGENCE, FL_ERR_SINGULAR, FL_ERR_CUDA = \
     0, -1, -2, -3, -4, -5
-FL_ROW_TILE, FL_COL_TILE, FL_ASM_TILE = 256, 32, 64
+FL_ROW_TILE, FL_COL_TILE, FL_ASM_TILE = 256, 32, 256
 FL_LSQR_SPLIT_MAX = 4
 FL_TBUILD_ROWS = 16
 

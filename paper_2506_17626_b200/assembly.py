@@ -23,6 +23,7 @@ import scipy.sparse
 
 from . import _device as D
 from . import _lib
+from ._featlsq import ref_assembly
 from .basis import ACTIVATIONS
 from .domains import support_runs
 from .errors import CapExceededError, CoverageError, InvalidInputError
@@ -31,14 +32,7 @@ from .jets import triples
 DENSE_SIZE_CAP = 20_000
 
 
-@dataclass(frozen=True)
-class SubdomainBlock:
-    """One subdomain's rows and columns of the global matrix (`assembly.py:43-50`)."""
-
-    subdomain: int
-    rows: np.ndarray
-    columns: np.ndarray
-    matrix: np.ndarray
+SubdomainBlock = ref_assembly.SubdomainBlock   # `assembly.py:43-50`
 
 
 class _BlockList(list):
@@ -119,12 +113,37 @@ class GlobalSystem:
         return self.csr().toarray()
 
 
+def adopt_system(system) -> GlobalSystem:
+    """A featlsq `GlobalSystem` with host blocks (`assembly.py:53-88`, e.g.
+    built by the reference `assemble` or by hand) as a device-resident
+    system: its blocks are uploaded once into a block store. Device systems
+    pass through unchanged."""
+    if isinstance(system, GlobalSystem):
+        return system
+    if not all(hasattr(system, a) for a in ("blocks", "rhs", "row_count", "column_count")):
+        raise InvalidInputError(f"cannot interpret {type(system)} as a GlobalSystem")
+    blocks = list(system.blocks)
+    k = system.basis.feature_count
+    for j, blk in enumerate(blocks):
+        if not np.array_equal(np.asarray(blk.columns), np.arange(j * k, (j + 1) * k)):
+            raise InvalidInputError(f"block {j} does not hold columns {j * k}..{(j + 1) * k - 1}")
+    store = D.blocks_from_host(system.row_count, [np.asarray(b.rows) for b in blocks],
+                               [np.asarray(b.matrix, dtype=float) for b in blocks])
+    out = GlobalSystem(system.problem, system.decomposition, system.basis,
+                       np.asarray(system.rhs, dtype=float), system.interior_count,
+                       system.row_count, system.column_count, system.lattice_axes,
+                       store=store, block_rows=[np.asarray(b.rows) for b in blocks])
+    out._blocks = _BlockList(blocks, out)
+    return out
+
+
 def apply(system: GlobalSystem, coeffs: np.ndarray) -> np.ndarray:
     """M a on the device (`assembly.py:91-96`)."""
     coeffs = np.asarray(coeffs, dtype=float)
     if coeffs.shape != (system.column_count,):
         raise InvalidInputError(
             f"coefficients must have shape ({system.column_count},), got {coeffs.shape}")
+    system = adopt_system(system)
     system.sync_device()
     return D.to_host(system.store.apply(D.to_dev(coeffs)))[:system.row_count]
 
@@ -135,6 +154,7 @@ def apply_transpose(system: GlobalSystem, residual: np.ndarray) -> np.ndarray:
     if residual.shape != (system.row_count,):
         raise InvalidInputError(
             f"residual must have shape ({system.row_count},), got {residual.shape}")
+    system = adopt_system(system)
     system.sync_device()
     return D.to_host(system.store.apply_t(D.to_dev(residual)))[:system.column_count]
 
@@ -509,36 +529,7 @@ def evaluate_solution(problem, dec, basis, coeffs, points) -> np.ndarray:
     return D.to_host(sb.predict_device(D.to_dev(coeffs)))
 
 
-@dataclass(frozen=True)
-class TestSet:
-    """Evaluation lattice with true values and their spread (`assembly.py:286-292`)."""
-
-    points: np.ndarray
-    true_values: np.ndarray
-    spread: float
-
-
-def make_test_set(problem, dec) -> TestSet:
-    """problem.test_points_per_count * count points per dimension
-    (`assembly.py:295-310`)."""
-    if problem.exact is None:
-        raise InvalidInputError(
-            f"problem {problem.name!r} has no exact or reference solution attached")
-    per_dim = problem.test_points_per_count * dec.count_per_dim
-    axes = [np.linspace(problem.domain.bounds[i, 0], problem.domain.bounds[i, 1], per_dim)
-            for i in range(problem.domain.dim)]
-    mesh = np.meshgrid(*axes, indexing="ij")
-    points = np.stack([m.ravel() for m in mesh], axis=1)
-    true_values = problem.exact(points)
-    spread = float(np.std(true_values))
-    if spread == 0.0:
-        raise InvalidInputError("true solution has zero spread on the test lattice")
-    return TestSet(points, true_values, spread)
-
-
-def l1_error(predicted, test_set: TestSet) -> float:
-    """Mean absolute error over the spread of the truth (`assembly.py:313-318`)."""
-    predicted = np.asarray(predicted, dtype=float)
-    if predicted.shape != test_set.true_values.shape:
-        raise InvalidInputError("prediction and truth shapes differ")
-    return float(np.mean(np.abs(predicted - test_set.true_values)) / test_set.spread)
+# featlsq's own test-lattice helpers (`assembly.py:286-318`)
+TestSet = ref_assembly.TestSet
+make_test_set = ref_assembly.make_test_set
+l1_error = ref_assembly.l1_error

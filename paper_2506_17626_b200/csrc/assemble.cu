@@ -1,27 +1,18 @@
 // K1 — fused block assembly (reference: featlsq assembly.py:124-238).
 //
-// One CTA per (block j, tile of FL_ASM_TILE rows). Phase 1: one thread per
-// row evaluates the point, the normalised partition-of-unity window jets
-// along every axis (domains.py:109-173: raw (1+cos)^2 factors, per-dim
-// normaliser summed over the covering centers in index order, jet quotient
-// jets.py:76-80, product over dims jets.py:55-63) and the normalised input
-// (basis.py:99-103) into shared memory. Phase 2: every thread produces
-// entries (row, k) for k = cg, cg+4, ...: tanh jet of the feature
-// (basis.py:119-126, jets.py:89-93), product rule with the window
-// (assembly.py:107-114), operator combination (problems.py:39-47) and row
-// weight (assembly.py:180-190), stored column-major so a warp writes 32
-// consecutive rows of one column (256 B, coalesced). Padding rows
-// [m_j, ld_j) are written as exact zeros.
+// One CTA per (block j, tile of FL_ASM_TILE = 256 rows), one row per thread;
+// see assemble_kernel below for the two phases. Padding rows [m_j, ld_j)
+// are written as exact zeros.
 //
-// Roofline: HBM write of 8 B per entry (plus a fp64 tanh per entry; see
-// DESIGN.md for the FP64 side).
+// Roofline: HBM write of 8 B per entry; the FP64 work per entry is one
+// reciprocal plus ~15 FMA-class instructions on the tabulated path
+// (DESIGN.md §3 K1).
 #include "common.cuh"
 
 namespace {
 
-constexpr int TILE = FL_ASM_TILE;
-constexpr int NT = 256;
-constexpr int CG = NT / TILE;  // column groups
+constexpr int NT = FL_ASM_TILE;
+static_assert(NT == 256, "one row per thread");
 constexpr int MAXD = 3;
 
 struct Jet {
@@ -63,15 +54,55 @@ __device__ __forceinline__ Jet raw_factor(double t, double mu, double half) {
   return r;
 }
 
-struct RowInfo {
-  double wv;              // window value
-  double wd1[MAXD];       // window d/dx_a
-  double wd2[MAXD];       // window d2/dx_a2
-  double xt[MAXD];        // normalised input
-  int coef;               // op_coef row (0 interior, 1+g constraint group)
-  int valid;
-};
+// tanh for |error| <= a few ulp of 1 (absolute): 1 - 2 / (exp(2x) + 1).
+// exp overflow gives rcp(inf) = 0 -> 1, underflow gives -1: no clamping.
+__device__ __forceinline__ double tanh_fast(double x) { return 1.0 - 2.0 * __drcp_rn(exp(2.0 * x) + 1.0); }
 
+// activation value and its first two derivatives at pre (basis.py:119-126)
+__device__ __forceinline__ void activation(int act, double pre, double& tv, double& g1, double& g2) {
+  if (act == FL_ACT_SIN) {
+    double sn, cs;
+    sincos(pre, &sn, &cs);
+    tv = sn;
+    g1 = cs;
+    g2 = -sn;
+  } else if (act == FL_ACT_SIGMOID) {
+    const double sg = 0.5 * (1.0 + tanh_fast(0.5 * pre));
+    tv = sg;
+    g1 = sg * (1.0 - sg);
+    g2 = sg * (1.0 - sg) * (1.0 - 2.0 * sg);
+  } else {
+    tv = tanh_fast(pre);
+    g1 = 1.0 - tv * tv;
+    g2 = -2.0 * tv * g1;
+  }
+}
+
+constexpr int CK = 32;        // columns per chunk
+constexpr int TLMAX = 192;    // lattice coordinates per chunk table (sum over axes)
+constexpr double EXP_SAFE = 300.0;  // |2 (x~ W + b)| bound of one table factor
+
+// One CTA per (block j, tile of NT rows), one row per thread.
+//
+// Phase 1 (per row): the point, the normalised partition-of-unity window
+// jets along every axis (domains.py:109-173: raw (1+cos)^2 factors,
+// normaliser over the covering centers in index order, jet quotient
+// jets.py:76-80, products jets.py:55-63, mask jets assembly.py:111-112),
+// folded with the operator coefficients (problems.py:39-47) and the row
+// weight (assembly.py:180-190) into
+//   entry(r, k) = t A_r + g1 sum_a fp_ka B_ra + g2 sum_a fp_ka^2 C_ra
+// with t, g1, g2 the activation jet of feature k at row r and fp_ka =
+// W_ka / h_a (basis.py:119-126; the product rule of assembly.py:107-114
+// regrouped by activation derivative).
+//
+// Phase 2 (per 32-column chunk): tanh features on an interior lattice box
+// use exp(2 (x~ . W_k + b_k)) = prod_a exp(2 (x~_a W_ka [+ b_k])): the
+// per-axis factors of the lattice coordinates the tile touches are
+// tabulated once per chunk (a few hundred exps for 8192 entries), so an
+// entry costs D - 1 multiplies, one reciprocal and ~12 FMAs; rows off the
+// lattice (constraint points), other activations and blocks whose factors
+// could overflow evaluate exp / sincos per entry. Stores are column-major:
+// a warp writes 32 consecutive rows of one column (256 B).
 template <int D>
 __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double* __restrict__ vals,
                                                       const int64_t* __restrict__ boff,
@@ -79,9 +110,11 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
                                                       const int32_t* __restrict__ bm) {
   extern __shared__ double smem[];
   const int K = d.nfeat;
-  double* sW = smem;              // (K, D)
-  double* sB = sW + K * D;        // (K)
-  __shared__ RowInfo rinfo[TILE];
+  double* tab = smem;            // (CK, TLMAX) exp table of one column chunk
+  double* sW = tab + CK * TLMAX; // (K, D)
+  double* sB = sW + K * D;       // (K)
+  double* sF1 = sB + K;          // (K, D) W / h
+  double* sF2 = sF1 + K * D;     // (K, D) (W / h)^2
   __shared__ double scoef[8][2 + 2 * MAXD];
 
   const int j = d.tiles[2 * blockIdx.x];
@@ -90,12 +123,24 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
   const int ld = bld[j];
   const int S = d.count_per_dim;
 
-  for (int i = threadIdx.x; i < K * D; i += NT) sW[i] = d.weights[(int64_t)j * K * D + i];
+  bool unsafe = false;
+  for (int i = threadIdx.x; i < K * D; i += NT) {
+    const int a = i % D;
+    const double w = d.weights[(int64_t)j * K * D + i];
+    const double fp = w * (1.0 / d.half[a]);
+    sW[i] = w;
+    sF1[i] = fp;
+    sF2[i] = fp * fp;
+    double e = fabs(2.0 * w);
+    if (a == 0) e += fabs(2.0 * d.biases[(int64_t)j * K + i / D]);
+    unsafe |= !(e <= EXP_SAFE);
+  }
   for (int i = threadIdx.x; i < K; i += NT) sB[i] = d.biases[(int64_t)j * K + i];
   if (threadIdx.x < 8 * (2 + 2 * D)) {
     int g = threadIdx.x / (2 + 2 * D), c = threadIdx.x % (2 + 2 * D);
     if (g <= d.ngroups) scoef[g][c] = d.op_coef[g * (2 + 2 * D) + c];
   }
+  __syncthreads();
 
   // subdomain multi-index (C order, domains.py:73-77)
   int sidx[MAXD];
@@ -106,125 +151,174 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
       rem /= S;
     }
   }
+  const int32_t* box = d.box + (int64_t)j * D * 2;
+  int boxcount = 1;
+  for (int i = 0; i < D; ++i) boxcount *= box[2 * i + 1];
 
-  if (threadIdx.x < TILE) {
-    const int r = r0 + threadIdx.x;
-    RowInfo ri;
-    ri.valid = 0;
-    ri.coef = 0;
-    if (r < m) {
-      ri.valid = 1;
-      double x[MAXD];
-      const int32_t* box = d.box + (int64_t)j * D * 2;
-      int boxcount = 1;
-      for (int i = 0; i < D; ++i) boxcount *= box[2 * i + 1];
-      const double* mk = nullptr;  // mask jets of this point, (D, 3)
-      if (r < boxcount) {
-        int rem = r;
-        int64_t gid = 0;
-        for (int i = D - 1; i >= 0; --i) {
-          int cnt = box[2 * i + 1];
-          int digit = rem % cnt;
-          rem /= cnt;
-          x[i] = d.axes[d.axis_off[i] + box[2 * i] + digit];
-          gid += (int64_t)(box[2 * i] + digit) * d.lattice_stride[i];
+  // lattice-coordinate ranges of this tile's box rows, per axis
+  int lo[MAXD], cnt[MAXD], base[MAXD];
+  int tl = 0;
+  const int rb1 = min(r0 + NT, min(boxcount, m));
+  bool use_tab = (d.activation == FL_ACT_TANH) && D >= 2 && rb1 > r0;
+  if (use_tab) {
+    int st = 1;
+    for (int a = D - 1; a >= 0; --a) {
+      const int n = box[2 * a + 1];
+      const int q0 = r0 / st, q1 = (rb1 - 1) / st;
+      int l = 0, c = n;
+      if (q1 - q0 < n) {
+        const int d0 = q0 % n, d1 = q1 % n;
+        if (d1 >= d0) {
+          l = d0;
+          c = d1 - d0 + 1;
         }
-        ri.coef = 0;
-        if (d.mask_int) mk = d.mask_int + gid * D * 3;
-      } else {
-        int64_t e = d.con_ptr[j] + (r - boxcount);
-        int pi = d.con_idx[e];
-        for (int i = 0; i < D; ++i) x[i] = d.con_pts[(int64_t)pi * D + i];
-        ri.coef = 1 + d.con_grp[e];
-        if (d.mask_con) mk = d.mask_con + (int64_t)pi * D * 3;
       }
-      // per-dim normalised factors: value-only and full jets
-      double fval[MAXD];
-      Jet ffull[MAXD];
-      for (int i = 0; i < D; ++i) {
-        const double* cen = d.centers + (int64_t)i * S;
-        const double half = d.half[i];
-        const double t = x[i];
-        Jet num = raw_factor(t, cen[sidx[i]], half);
-        Jet den{0.0, 0.0, 0.0};
-        int lo = sidx[i] - d.reach, hi = sidx[i] + d.reach;
-        if (lo < 0) lo = 0;
-        if (hi > S - 1) hi = S - 1;
-        for (int s = lo; s <= hi; ++s) {  // non-covering centers add exact zeros
-          Jet f = raw_factor(t, cen[s], half);
-          den.v += f.v;
-          den.f += f.f;
-          den.s += f.s;
-        }
-        Jet q = jmul(num, jrecip(den));
-        ffull[i] = q;
-        Jet numv{num.v, 0.0, 0.0}, denv{den.v, 0.0, 0.0};
-        fval[i] = jmul(numv, jrecip(denv)).v;
-        ri.xt[i] = (t - cen[sidx[i]]) / half;
-      }
-      for (int a = 0; a < D; ++a) {
-        Jet w{0.0, 0.0, 0.0};
-        for (int i = 0; i < D; ++i) {
-          Jet fi = (i == a) ? ffull[i] : Jet{fval[i], 0.0, 0.0};
-          w = (i == 0) ? fi : jmul(w, fi);
-        }
-        if (mk) w = jmul(w, Jet{mk[3 * a], mk[3 * a + 1], mk[3 * a + 2]});  // window * mask (assembly.py:111-112)
-        if (a == 0) ri.wv = w.v;
-        ri.wd1[a] = w.f;
-        ri.wd2[a] = w.s;
-      }
+      lo[a] = l;
+      cnt[a] = c;
+      st *= n;
     }
-    rinfo[threadIdx.x] = ri;
+    for (int a = 0; a < D; ++a) {
+      base[a] = tl;
+      tl += cnt[a];
+    }
+    use_tab = tl <= TLMAX;
   }
-  __syncthreads();
 
-  const int tr = threadIdx.x % TILE;
-  const int cg = threadIdx.x / TILE;
-  const int r = r0 + tr;
-  if (r >= ld) return;
-  double* out = vals + boff[j] + r;
-  const RowInfo& ri = rinfo[tr];
-  if (!ri.valid) {
-    for (int k = cg; k < K; k += CG) out[(int64_t)k * ld] = 0.0;
-    return;
+  // ---- phase 1: this thread's row ----
+  const int r = r0 + threadIdx.x;
+  bool valid = r < m, on_box = false;
+  double A = 0.0, Bc[MAXD], Cc[MAXD], xt[MAXD];
+  int tix[MAXD];
+  for (int a = 0; a < MAXD; ++a) {
+    Bc[a] = Cc[a] = xt[a] = 0.0;
+    tix[a] = 0;
   }
-  double invh[MAXD];
-  for (int a = 0; a < D; ++a) invh[a] = 1.0 / d.half[a];
-  const double* co = scoef[ri.coef];
-  const double vcoef = co[0], weight = co[1];
-  for (int k = cg; k < K; k += CG) {
-    double pre = ri.xt[0] * sW[k * D + 0];
-    for (int i = 1; i < D; ++i) pre += ri.xt[i] * sW[k * D + i];
-    pre += sB[k];
-    double tv, g1, g2;  // activation value, first and second derivative
-    if (d.activation == FL_ACT_TANH) {
-      tv = tanh(pre);
-      g1 = 1.0 - tv * tv;
-      g2 = -2.0 * tv * g1;
-    } else if (d.activation == FL_ACT_SIN) {
-      double sn, cs;
-      sincos(pre, &sn, &cs);
-      tv = sn;
-      g1 = cs;
-      g2 = -sn;
+  if (valid) {
+    double x[MAXD];
+    const double* mk = nullptr;  // mask jets of this point, (D, 3)
+    int coef = 0;
+    if (r < boxcount) {
+      int rem = r;
+      int64_t gid = 0;
+      for (int i = D - 1; i >= 0; --i) {
+        const int n = box[2 * i + 1];
+        const int digit = rem % n;
+        rem /= n;
+        x[i] = d.axes[d.axis_off[i] + box[2 * i] + digit];
+        gid += (int64_t)(box[2 * i] + digit) * d.lattice_stride[i];
+        tix[i] = digit;
+      }
+      on_box = true;
+      if (d.mask_int) mk = d.mask_int + gid * D * 3;
     } else {
-      double sg = 0.5 * (1.0 + tanh(0.5 * pre));
-      tv = sg;
-      g1 = sg * (1.0 - sg);
-      g2 = sg * (1.0 - sg) * (1.0 - 2.0 * sg);
+      const int64_t e = d.con_ptr[j] + (r - boxcount);
+      const int pi = d.con_idx[e];
+      for (int i = 0; i < D; ++i) x[i] = d.con_pts[(int64_t)pi * D + i];
+      coef = 1 + d.con_grp[e];
+      if (d.mask_con) mk = d.mask_con + (int64_t)pi * D * 3;
     }
+    // per-dim normalised factors: value-only and full jets
+    double fval[MAXD];
+    Jet ffull[MAXD];
+    for (int i = 0; i < D; ++i) {
+      const double* cen = d.centers + (int64_t)i * S;
+      const double half = d.half[i];
+      const double t = x[i];
+      Jet num = raw_factor(t, cen[sidx[i]], half);
+      Jet den{0.0, 0.0, 0.0};
+      int l = sidx[i] - d.reach, h = sidx[i] + d.reach;
+      if (l < 0) l = 0;
+      if (h > S - 1) h = S - 1;
+      for (int s2 = l; s2 <= h; ++s2) {  // non-covering centers add exact zeros
+        Jet f = raw_factor(t, cen[s2], half);
+        den.v += f.v;
+        den.f += f.f;
+        den.s += f.s;
+      }
+      ffull[i] = jmul(num, jrecip(den));
+      Jet numv{num.v, 0.0, 0.0}, denv{den.v, 0.0, 0.0};
+      fval[i] = jmul(numv, jrecip(denv)).v;
+      xt[i] = (t - cen[sidx[i]]) / half;
+    }
+    const double* co = scoef[coef];
+    const double weight = co[1];
+    double wv = 0.0;
     double acc = 0.0;
     for (int a = 0; a < D; ++a) {
-      double fp = sW[k * D + a] * invh[a];
-      double f1 = g1 * fp;
-      double f2 = g2 * fp * fp;
-      double v = ri.wv * tv;
-      double d1 = ri.wd1[a] * tv + ri.wv * f1;
-      double d2 = ri.wd2[a] * tv + 2.0 * ri.wd1[a] * f1 + ri.wv * f2;
-      if (a == 0) acc = vcoef * v;
-      acc = acc + co[2 + a] * d1 + co[2 + D + a] * d2;
+      Jet w{0.0, 0.0, 0.0};
+      for (int i = 0; i < D; ++i) {
+        Jet fi = (i == a) ? ffull[i] : Jet{fval[i], 0.0, 0.0};
+        w = (i == 0) ? fi : jmul(w, fi);
+      }
+      if (mk) w = jmul(w, Jet{mk[3 * a], mk[3 * a + 1], mk[3 * a + 2]});
+      if (a == 0) {
+        wv = w.v;
+        acc = co[0] * wv;
+      }
+      const double c1 = co[2 + a], c2 = co[2 + D + a];
+      acc += c1 * w.f + c2 * w.s;
+      Bc[a] = weight * (c1 * wv + 2.0 * c2 * w.f);
+      Cc[a] = weight * (c2 * wv);
     }
-    out[(int64_t)k * ld] = acc * weight;
+    A = weight * acc;
+  }
+  unsafe = __syncthreads_or(unsafe);
+  use_tab = use_tab && !unsafe;
+  const bool store = r < ld;  // rows past the padding only help build the tables
+  double* out = vals + boff[j] + r;
+  int toff[MAXD];
+  for (int a = 0; a < D; ++a) toff[a] = base[a] + tix[a] - lo[a];
+  const bool row_tab = use_tab && on_box;
+
+  // ---- phase 2: 32-column chunks ----
+  for (int k0 = 0; k0 < K; k0 += CK) {
+    const int nk = min(CK, K - k0);
+    if (use_tab) {
+      __syncthreads();
+      // tab[c * TLMAX + base_a + i] = exp(2 (x~_a(i) W_{k0+c, a} [+ b]))
+      for (int p = threadIdx.x; p < nk * tl; p += NT) {
+        const int c = p / tl, q = p % tl;
+        int a = 0;
+        while (a + 1 < D && q >= base[a + 1]) ++a;
+        const int digit = lo[a] + (q - base[a]);
+        const double xa = (d.axes[d.axis_off[a] + box[2 * a] + digit] - d.centers[(int64_t)a * S + sidx[a]]) /
+                          d.half[a];
+        double e = xa * sW[(k0 + c) * D + a];
+        if (a == 0) e += sB[k0 + c];
+        tab[c * TLMAX + q] = exp(2.0 * e);
+      }
+      __syncthreads();
+    }
+    if (!store) continue;
+    if (!valid) {
+      for (int c = 0; c < nk; ++c) out[(int64_t)(k0 + c) * ld] = 0.0;
+      continue;
+    }
+    for (int c = 0; c < nk; ++c) {
+      const int k = k0 + c;
+      double tv, g1, g2;
+      if (row_tab) {
+        double E = tab[c * TLMAX + toff[0]];
+#pragma unroll
+        for (int a = 1; a < D; ++a) E *= tab[c * TLMAX + toff[a]];
+        tv = 1.0 - 2.0 * __drcp_rn(E + 1.0);
+        g1 = 1.0 - tv * tv;
+        g2 = -2.0 * tv * g1;
+      } else {
+        double pre = xt[0] * sW[k * D + 0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) pre += xt[i] * sW[k * D + i];
+        pre += sB[k];
+        activation(d.activation, pre, tv, g1, g2);
+      }
+      double p1 = sF1[k * D] * Bc[0], p2 = sF2[k * D] * Cc[0];
+#pragma unroll
+      for (int a = 1; a < D; ++a) {
+        p1 += sF1[k * D + a] * Bc[a];
+        p2 += sF2[k * D + a] * Cc[a];
+      }
+      out[(int64_t)k * ld] = tv * A + g1 * p1 + g2 * p2;
+    }
   }
 }
 
@@ -234,8 +328,8 @@ extern "C" int fl_assemble(const fl_assembly_desc* desc, const fl_blockop* out, 
   if (desc->dim < 1 || desc->dim > MAXD || desc->ngroups > 7) return FL_ERR_INVALID;
   if (desc->n_tiles == 0) return FL_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  size_t smem = (size_t)desc->nfeat * (desc->dim + 1) * sizeof(double);
-  if (smem > 200 * 1024) return FL_ERR_INVALID;
+  size_t smem = ((size_t)desc->nfeat * (3 * desc->dim + 1) + CK * TLMAX) * sizeof(double);
+  if (smem > 220 * 1024) return FL_ERR_INVALID;
   switch (desc->dim) {
     case 1:
       cudaFuncSetAttribute(assemble_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

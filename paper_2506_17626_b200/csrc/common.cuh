@@ -6,6 +6,18 @@
 #include "../../include/featlsq_b200.h"
 
 namespace fl {
+
+// true the first time it is called for the current device with this flag
+// word (per-device one-time setup such as cudaFuncSetAttribute)
+inline bool first_on_device(unsigned long long& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (seen & bit) return false;
+  seen |= bit;
+  return true;
+}
+
 // thread-local description of the last failure (fl_last_error)
 void set_error(const char* file, int line, cudaError_t e);
 }  // namespace fl

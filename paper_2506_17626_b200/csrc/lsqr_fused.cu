@@ -41,16 +41,9 @@
 #ifndef ROW_CTAS_PER_SM
 #define ROW_CTAS_PER_SM 3
 #endif
-#ifndef FL_Q_EVICT_FIRST
-// 1: Q's TMA loads with an L2 evict_first policy. Measured on cfg4: 1.444 vs
-// 1.423-1.429 ms per iteration (the row kernel still reads its 66 MB from DRAM)
-#define FL_Q_EVICT_FIRST 0
-#endif
-#ifndef FL_PARTIAL_EVICT_LAST
-// 1: partial-product stores with an L2 evict_last policy (for the row
-// kernel's gather). Measured on cfg4: 1.416 vs 1.399 ms per iteration: off.
-#define FL_PARTIAL_EVICT_LAST 0
-#endif
+// Measured and removed (DESIGN.md §3 K4): an L2 evict_first policy on the Q
+// stream (1.444 vs 1.423 ms per iteration on cfg4) and an evict_last policy
+// on the partial-product stores (1.416 vs 1.399 ms).
 
 namespace {
 
@@ -139,20 +132,9 @@ __global__ void __launch_bounds__(NT, MB)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
     const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (k % SL) * ldmax);
-#if FL_Q_EVICT_FIRST
-    // Q is read once per iteration (9 GB >> L2): evict it first so the
-    // partials, u and the vectors stay in L2 for the row kernel
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
-        "l"(Q + (int64_t)(cbeg + k) * ld), "r"(bytes), "r"(bar), "l"(pol)
-        : "memory");
-#else
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
                  "l"(Q + (int64_t)(cbeg + k) * ld), "r"(bytes), "r"(bar)
                  : "memory");
-#endif
   };
   auto wait_col = [&](int k) {
     const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[k % SL]);
@@ -293,26 +275,12 @@ __global__ void __launch_bounds__(NT, MB)
         }
       }
     }
-#if FL_PARTIAL_EVICT_LAST
-    // the row kernel gathers these right after this kernel: keep them in L2
-    // while the Q stream passes through
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
-#endif
 #pragma unroll
     for (int i = 0; i < RP; ++i) {
       const int r = 2 * (threadIdx.x + i * NT);
       double* pout = op.partial + h * op.partial_len + op.row_off[j];
-#if FL_PARTIAL_EVICT_LAST
-      if (r < m)
-        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(pout + r), "d"(pp_r[i].x), "l"(pol) : "memory");
-      if (r + 1 < m)
-        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(pout + r + 1), "d"(pp_r[i].y), "l"(pol)
-                     : "memory");
-#else
       if (r < m) pout[r] = pp_r[i].x;
       if (r + 1 < m) pout[r + 1] = pp_r[i].y;
-#endif
     }
   }
   // ---- grid reductions: alpha^2, w^2, non-finite ----
@@ -527,8 +495,12 @@ template <int NT, int RP, int W, int ST, int MB>
 int try_fused(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64_t it, int mode, int ldmax,
               int S, cudaStream_t s, bool dry) {
   if ((int64_t)2 * RP * NT < ldmax) return SKIP;
+  // cudaFuncSetAttribute is per device: cache the raised limit per device id
   static int stat = -1;
-  static size_t attr = 0;
+  static size_t attr_dev[64] = {};
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  size_t& attr = attr_dev[dev & 63];
   if (stat < 0) {
     cudaFuncAttributes a;
     FL_CUDA(cudaFuncGetAttributes(&a, fused_kernel<NT, RP, W, ST, MB>));

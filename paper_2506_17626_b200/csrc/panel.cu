@@ -369,10 +369,9 @@ __global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
 namespace fl {
 int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t* m, int J, int K, int P0,
                  double* tau, double* T, cudaStream_t s, const double* src) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (fl::first_on_device(attr)) {
     FL_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_S));
-    attr = true;
   }
   PanelArgs a{A, off, ld, m, K, P0, tau, T, src};
   panel_kernel<<<J, NT, SMEM_S, s>>>(a);

@@ -78,7 +78,6 @@ struct QfArgs {
   const double* T64;     // (J, K/64, 64, 64) column-major upper-triangular T_b
   int K;
   int tiles_per_block;
-  const int32_t* nrefl;  // reflectors per block (null: all K); blocks past it are identities
 };
 
 __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
@@ -99,8 +98,7 @@ __global__ void __launch_bounds__(NT, QF_MINB) qform_kernel(QfArgs a) {
   const double* V = a.V + (a.voff ? a.voff[j] : (int64_t)j * K * K);
   double* C = a.C + (a.coff ? a.coff[j] : (int64_t)j * K * K) + (int64_t)c0 * cld;
   const double* Tj = a.T64 + (int64_t)j * (K / NB) * NB * NB;
-  const int nr = a.nrefl ? min(a.nrefl[j], mj) : mj;
-  const int nact = min(K / NB, (nr + NB - 1) / NB);  // blocks with reflectors
+  const int nact = min(K / NB, (mj + NB - 1) / NB);  // blocks with reflectors
   if (nact <= 0) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
@@ -312,14 +310,13 @@ namespace fl {
 // Q (blocks at coff/cld, holding [Q1; 0]) <- Q0 Q for every block; K % 64 == 0.
 int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
                 const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int K, int J,
-                cudaStream_t s, const int32_t* nrefl) {
+                cudaStream_t s) {
   if (K % NB) return FL_ERR_INVALID;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (fl::first_on_device(attr)) {
     FL_CUDA(cudaFuncSetAttribute(qform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr = true;
   }
-  QfArgs a{V, voff, vld, m, C, coff, cld, rank, T64, K, (K + TN - 1) / TN, nrefl};
+  QfArgs a{V, voff, vld, m, C, coff, cld, rank, T64, K, (K + TN - 1) / TN};
   qform_kernel<<<J * a.tiles_per_block, NT, SMEM, s>>>(a);
   FL_CHECK_LAUNCH();
   return FL_OK;
@@ -333,5 +330,5 @@ extern "C" int fl_dev_qform(const double* V, const int64_t* voff, const int32_t*
                             int32_t K, int32_t nblocks, void* stream) {
   if (nblocks == 0) return FL_OK;
   if (!voff || !vld || !coff || !cld) return FL_ERR_INVALID;
-  return fl::qform_fused(V, voff, vld, m, C, coff, cld, rank, T64, K, nblocks, (cudaStream_t)stream, nullptr);
+  return fl::qform_fused(V, voff, vld, m, C, coff, cld, rank, T64, K, nblocks, (cudaStream_t)stream);
 }

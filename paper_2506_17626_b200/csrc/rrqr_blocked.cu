@@ -11,7 +11,6 @@
 // per-block size that depends on the rank is read by the kernels from device
 // memory (tiles past r_j exit immediately).
 #include <float.h>
-#include <stdlib.h>
 
 #include "wy.cuh"
 
@@ -20,15 +19,12 @@ int panel_factor(double* A, const int64_t* off, const int32_t* ld, const int32_t
                  double* tau, double* T, cudaStream_t s, const double* src = nullptr);
 int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
             int32_t* rank, double* diag, cudaStream_t s);
-bool qrcp2_ok(int K);
-int qrcp2_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double* tau, int32_t* perm,
-             int32_t* rank, double* diag, cudaStream_t s);
 int wy_apply(const WyArgs& a, cudaStream_t s);
 int wy_nb();
 int wy_tn();
 int qform_fused(const double* V, const int64_t* voff, const int32_t* vld, const int32_t* m, double* C,
                 const int64_t* coff, const int32_t* cld, const int32_t* rank, const double* T64, int K, int J,
-                cudaStream_t s, const int32_t* nrefl = nullptr);
+                cudaStream_t s);
 }  // namespace fl
 
 namespace {
@@ -36,10 +32,14 @@ namespace {
 constexpr int NB = 32;
 constexpr int NT = 256;
 
-// R0w[j] (K x K, ld K) = upper triangle of the factored work block's top K rows
+// R0w[j] (K x K, ld K) = upper triangle of the factored work block's top K rows.
+// bad[j] != 0 when R0_j holds a non-finite entry: a NaN/Inf anywhere in A_j
+// reaches R0_j (every reflector dot product over a non-finite column is
+// non-finite, 0 * Inf included), so this is the `_check_matrix` test of
+// linalg.py:49-55 for the blocked route.
 __global__ void extract_r0_kernel(const double* __restrict__ W, const int64_t* __restrict__ off,
                                   const int32_t* __restrict__ ld, const int32_t* __restrict__ m, int K,
-                                  double* __restrict__ R0, int32_t* __restrict__ kmax) {
+                                  double* __restrict__ R0, int32_t* __restrict__ kmax, int32_t* __restrict__ bad) {
   const int j = blockIdx.y;
   const int64_t n = (int64_t)K * K;
   const int mj = m[j];
@@ -47,8 +47,16 @@ __global__ void extract_r0_kernel(const double* __restrict__ W, const int64_t* _
   if (blockIdx.x == 0 && threadIdx.x == 0) kmax[j] = km;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(p / K), r = (int)(p % K);
-    R0[(int64_t)j * n + p] = (r <= c && r < km) ? W[off[j] + (int64_t)c * ld[j] + r] : 0.0;
+    const double v = (r <= c && r < km) ? W[off[j] + (int64_t)c * ld[j] + r] : 0.0;
+    if (!isfinite(v)) bad[j] = 1;
+    R0[(int64_t)j * n + p] = v;
   }
+}
+
+// blocks with a non-finite entry report rank -1 (the host raises InvalidInputError)
+__global__ void mark_nonfinite_kernel(const int32_t* __restrict__ bad, int J, int32_t* __restrict__ rank) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < J && bad[j]) rank[j] = -1;
 }
 
 // per (block, panel of the QRCP reflectors): T from G = V^T V (V unit lower in
@@ -170,12 +178,10 @@ __global__ void __launch_bounds__(NT) combine_t_kernel(const double* __restrict_
   __shared__ double V2s[NB * GLD];
   __shared__ double Xs[NB * NB];
   __shared__ double Ys[NB * NB];
-  if (q < 0) q = blockIdx.x;  // all 64-blocks in one launch
   const int j = blockIdx.y, P0 = 64 * q;
   const int npan32 = K / NB, npan64 = K / 64;
-  // off / ld may be null: the (J, K, K) factor R0 (stride K * K, ld K)
-  const double* A = W + (off ? off[j] : (int64_t)j * K * K);
-  const int64_t ldj = ld ? ld[j] : K;
+  const double* A = W + off[j];
+  const int64_t ldj = ld[j];
   const int M = m[j] - (P0 + NB);  // rows of V2's support
   const double* T1 = T32 + ((int64_t)j * npan32 + 2 * q) * NB * NB;
   const double* T2 = T1 + NB * NB;
@@ -270,8 +276,8 @@ __global__ void clamp_tau_kernel(double* tau, int K, const int32_t* rank) {
 
 namespace {
 struct Workspace {
-  double *fac, *R0, *Q1, *T0, *T1, *T64, *T164, *tau0, *tau1;
-  int32_t* kmax;
+  double *fac, *R0, *Q1, *T0, *T1, *T64, *tau0, *tau1;
+  int32_t *kmax, *bad;
 };
 
 Workspace carve(void* base, int J, int K, int64_t store_elems, size_t* total) {
@@ -290,10 +296,10 @@ Workspace carve(void* base, int J, int K, int64_t store_elems, size_t* total) {
   ws.T0 = (double*)take((size_t)J * npan * NB * NB * 8);
   ws.T1 = (double*)take((size_t)J * npan * NB * NB * 8);
   ws.T64 = (double*)take((size_t)J * (K / 64 + 1) * 64 * 64 * 8);
-  ws.T164 = (double*)take((size_t)J * (K / 64) * 64 * 64 * 8);  // 64-wide T of the QRCP reflectors
   ws.tau0 = (double*)take((size_t)J * K * 8);
   ws.tau1 = (double*)take((size_t)J * K * 8);
   ws.kmax = (int32_t*)take((size_t)J * 4);
+  ws.bad = (int32_t*)take((size_t)J * 4);
   if (total) *total = used;
   return ws;
 }
@@ -329,10 +335,9 @@ extern "C" int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t
 }
 
 namespace {
-// The whole route for the J blocks of one group; A, Q, R, perm, rank, diag
-// and the workspace arrays are already offset to the group's first block.
-int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, double* R, int32_t* perm,
-              int32_t* rank, double* diag, const Workspace& ws, int J, cudaStream_t s, cudaEvent_t k2a_done) {
+// The whole route for the J blocks of one store.
+int run_route(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, double* R, int32_t* perm,
+              int32_t* rank, double* diag, const Workspace& ws, int J, cudaStream_t s) {
   const int npan = K / NB;
   const int TN = fl::wy_tn();
   const bool wide = (K % 64) == 0;  // 64-wide compact-WY updates
@@ -377,48 +382,19 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
       }
     }
   }
-  if (k2a_done) FL_CUDA(cudaEventRecord(k2a_done, s));
   // ---- K2b: truncated QRCP of R0 ----
-  extract_r0_kernel<<<dim3(64, J), 256, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.R0, ws.kmax);
+  FL_CUDA(cudaMemsetAsync(ws.bad, 0, (size_t)J * sizeof(int32_t), s));
+  extract_r0_kernel<<<dim3(64, J), 256, 0, s>>>(fac, A->off, A->ld, A->m, K, ws.R0, ws.kmax, ws.bad);
   FL_CHECK_LAUNCH();
-  static const int q2 = [] {
-    const char* e = getenv("FEATLSQ_QRCP2");
-    return e ? atoi(e) : 0;
-  }();
-  if (q2 && fl::qrcp2_ok(K)) {
-    if ((e = fl::qrcp2_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) return e;
-  } else if ((e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) {
-    return e;
-  }
+  if ((e = fl::qrcp_r0(ws.R0, K, ws.kmax, J, sigma, ws.tau1, perm, rank, diag, s))) return e;
   clamp_tau_kernel<<<J, 256, 0, s>>>(ws.tau1, K, rank);
   build_t_kernel<<<dim3(npan, J), NT, 0, s>>>(ws.R0, K, ws.kmax, ws.tau1, rank, ws.T1);
   init_q1_r_kernel<<<dim3(64, J), 256, 0, s>>>(ws.R0, K, rank, ws.Q1, R);
   FL_CHECK_LAUNCH();
-  // ---- Q1 = H'_0 .. H'_{r-1} [S; 0] ----
-  static const int qf = [] {
-    const char* e = getenv("FEATLSQ_QFORM");  // 0: two-pass wy_apply per reflector block
-    return e ? atoi(e) : 1;
-  }();
-  static const int qf1 = [] {
-    const char* e = getenv("FEATLSQ_QFORM_Q1");
-    return e ? atoi(e) : 0;
-  }();
-  if (wide && qf1) {
-    // opt-in: 64-wide T of the QRCP reflectors, then the fused sweep
-    // (qform.cu) over the first ceil(r / 64) reflector blocks only (tau is 0
-    // past the rank). Measured on cfg4: 12.7 ms per filter (combine 1.3 +
-    // sweep 11.4) against 8.5 for the 32-wide two-pass launches on these
-    // 512-row blocks, whose passes are too short for the fused kernel.
-    // Covered by the parity tests when enabled (82 passed).
-    combine_t_kernel<<<dim3(K / 64, J), NT, 0, s>>>(ws.R0, nullptr, nullptr, ws.kmax, K, ws.T1, ws.T164, -1);
-    FL_CHECK_LAUNCH();
-    if ((e = fl::qform_fused(ws.R0, nullptr, nullptr, ws.kmax, ws.Q1, nullptr, nullptr, rank, ws.T164, K, J, s,
-                             rank)))
-      return e;
-  } else
-  // panels in reverse, columns >= P0 only (measured: 64-wide blocks with
-  // combined T's, 9.95 ms per filter incl. the combine, vs 8.3 for these
-  // 32-wide launches on the 512-row factors)
+  // ---- Q1 = H'_0 .. H'_{r-1} [S; 0]: 32-wide panels in reverse, columns >= P0 ----
+  // (measured: 64-wide blocks with combined T's 9.95 ms per filter incl. the
+  // combine, the fused qform sweep 12.7 ms, vs 8.3 for these launches on the
+  // 512-row factors, whose passes are too short for the wider kernels)
   for (int p = npan - 1; p >= 0; --p) {
     const int P0 = p * NB;
     fl::WyArgs a{};
@@ -442,55 +418,43 @@ int run_group(const fl_blockop* A, const fl_blockop* Q, int K, double sigma, dou
     if ((e = fl::wy_apply_nb(a, 32, s))) return e;
   }
   // ---- K2c: Qhat = Q0 [Q1; 0], reflector blocks of Q0 in reverse ----
-  init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, Q->m, (wide && qf) ? 1 : 0,
+  init_qhat_kernel<<<dim3(128, J), 256, 0, s>>>(ws.Q1, K, rank, Q->off, Q->ld, Q->m, wide ? 1 : 0,
                                                 (double*)Q->vals);
   FL_CHECK_LAUNCH();
-  if (wide && qf) return fl::qform_fused(fac, A->off, A->ld, A->m, (double*)Q->vals, Q->off, Q->ld, rank, ws.T64, K, J, s);
-  const int wb = wide ? 64 : NB;
-  for (int p = K / wb - 1; p >= 0; --p) {
-    const int P0 = p * wb;
-    fl::WyArgs a{};
-    a.V = fac;
-    a.voff = A->off;
-    a.vld = A->ld;
-    a.C = (double*)Q->vals;
-    a.coff = Q->off;
-    a.cld = Q->ld;
-    a.m = A->m;
-    a.T = wide ? ws.T64 + (int64_t)p * 64 * 64 : ws.T0 + (int64_t)p * NB * NB;
-    a.tstride = wide ? t64s : t32s;
-    a.v_col0 = P0;
-    a.c_col0 = 0;
-    a.row0 = P0;
-    a.transT = 0;
-    a.ncols = rank;
-    a.ncols_sub = 0;
-    a.tiles_per_block = (K + TN - 1) / TN;
-    a.ntiles = J * a.tiles_per_block;
-    if ((e = fl::wy_apply_nb(a, wb, s))) return e;
+  if (wide) {
+    // one fused sweep per 64-column tile of Qhat (qform.cu)
+    if ((e = fl::qform_fused(fac, A->off, A->ld, A->m, (double*)Q->vals, Q->off, Q->ld, rank, ws.T64, K, J, s)))
+      return e;
+  } else {
+    for (int p = K / NB - 1; p >= 0; --p) {
+      const int P0 = p * NB;
+      fl::WyArgs a{};
+      a.V = fac;
+      a.voff = A->off;
+      a.vld = A->ld;
+      a.C = (double*)Q->vals;
+      a.coff = Q->off;
+      a.cld = Q->ld;
+      a.m = A->m;
+      a.T = ws.T0 + (int64_t)p * NB * NB;
+      a.tstride = t32s;
+      a.v_col0 = P0;
+      a.c_col0 = 0;
+      a.row0 = P0;
+      a.transT = 0;
+      a.ncols = rank;
+      a.ncols_sub = 0;
+      a.tiles_per_block = (K + TN - 1) / TN;
+      a.ntiles = J * a.tiles_per_block;
+      if ((e = fl::wy_apply_nb(a, NB, s))) return e;
+    }
   }
+  mark_nonfinite_kernel<<<(J + 255) / 256, 256, 0, s>>>(ws.bad, J, rank);
+  FL_CHECK_LAUNCH();
   return FL_OK;
-}
-
-constexpr int MAX_GROUPS = 8;
-cudaStream_t g_streams[MAX_GROUPS] = {};
-
-int group_count(int J) {
-  const char* e = getenv("FEATLSQ_RRQR_GROUPS");
-  // default one group: all blocks in every launch (measured on cfg4: 373 ms
-  // per filter vs 390 ms with 2 or 4 staggered groups — the groups did not
-  // overlap, and a 256-block launch of K2b or the panel kernel is 1.7 waves)
-  int g = e ? atoi(e) : 1;
-  if (g < 1) g = 1;
-  if (g > MAX_GROUPS) g = MAX_GROUPS;
-  while (g > 1 && J / g < 32) --g;  // keep every group a full wave of blocks
-  return g;
 }
 }  // namespace
 
-// Blocks are split into G groups, each run through the whole route on its own
-// stream, group g+1 starting when group g has finished K2a: the latency- and
-// HBM-bound K2b of one group overlaps the DMMA-bound K2a/K2c of the others.
 extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,
                                double sigma, double* R, int32_t* perm, int32_t* rank, double* diag,
                                void* workspace, void* stream) {
@@ -498,53 +462,9 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
   const int J = A->nblocks;
   if (J == 0) return FL_OK;
   // shared-memory bounds of K2a (>= 2 staged panel columns) and K2b (F panel)
-  if (A->max_rows > 11776 || K > 640) return FL_ERR_INVALID;
-  cudaStream_t s = (cudaStream_t)stream;
+  if (A->max_rows > FL_RRQR_BLOCKED_MAX_ROWS || K > FL_RRQR_BLOCKED_MAX_K) return FL_ERR_INVALID;
   Workspace ws = carve(workspace, J, K, store_elems, nullptr);
   // the raw blocks stay intact: the first K2a step reads them and writes the
   // factor copy (same layout, absolute offsets)
-  const int G = group_count(J);
-  if (G == 1) return run_group(A, Q, K, sigma, R, perm, rank, diag, ws, J, s, nullptr);
-
-  const int64_t kk = (int64_t)K * K, t32s = (int64_t)(K / NB) * NB * NB, t64s = (int64_t)(K / 64) * 64 * 64;
-  cudaEvent_t start, k2a[MAX_GROUPS], done[MAX_GROUPS];
-  FL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  FL_CUDA(cudaEventRecord(start, s));
-  int err = FL_OK;
-  for (int g = 0; g < G && !err; ++g) {
-    if (!g_streams[g]) FL_CUDA(cudaStreamCreateWithFlags(&g_streams[g], cudaStreamNonBlocking));
-    FL_CUDA(cudaEventCreateWithFlags(&k2a[g], cudaEventDisableTiming));
-    FL_CUDA(cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming));
-    const int j0 = (int)((int64_t)J * g / G), j1 = (int)((int64_t)J * (g + 1) / G), Jg = j1 - j0;
-    cudaStream_t sg = g_streams[g];
-    FL_CUDA(cudaStreamWaitEvent(sg, start, 0));
-    if (g > 0) FL_CUDA(cudaStreamWaitEvent(sg, k2a[g - 1], 0));
-    fl_blockop Ag = *A, Qg = *Q;
-    Ag.nblocks = Qg.nblocks = Jg;
-    Ag.off += j0;
-    Ag.ld += j0;
-    Ag.m += j0;
-    Qg.off += j0;
-    Qg.ld += j0;
-    Qg.m += j0;
-    Workspace wg = ws;
-    wg.R0 += j0 * kk;
-    wg.Q1 += j0 * kk;
-    wg.T0 += j0 * t32s;
-    wg.T1 += j0 * t32s;
-    wg.T64 += j0 * t64s;
-    wg.tau0 += (int64_t)j0 * K;
-    wg.tau1 += (int64_t)j0 * K;
-    wg.kmax += j0;
-    err = run_group(&Ag, &Qg, K, sigma, R + j0 * kk, perm + (int64_t)j0 * K, rank + j0, diag + (int64_t)j0 * K,
-                    wg, Jg, sg, k2a[g]);
-    FL_CUDA(cudaEventRecord(done[g], sg));
-    FL_CUDA(cudaStreamWaitEvent(s, done[g], 0));
-  }
-  cudaEventDestroy(start);
-  for (int g = 0; g < G; ++g) {
-    cudaEventDestroy(k2a[g]);
-    cudaEventDestroy(done[g]);
-  }
-  return err;
+  return run_route(A, Q, K, sigma, R, perm, rank, diag, ws, J, (cudaStream_t)stream);
 }

@@ -277,11 +277,10 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
 
 template <int NB>
 int launch(const fl::WyArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (fl::first_on_device(attr)) {
     FL_CUDA(cudaFuncSetAttribute(wy_apply_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Cfg<NB>::smem));
-    attr = true;
   }
   wy_apply_kernel<NB><<<a.ntiles, Cfg<NB>::NT, Cfg<NB>::smem, s>>>(a);
   FL_CHECK_LAUNCH();

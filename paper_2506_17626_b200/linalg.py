@@ -7,48 +7,20 @@ is K5 on one block.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
-
 import numpy as np
 
 from . import _device as D
 from . import _lib
+from ._featlsq import ref_assembly, ref_linalg
 from .errors import InvalidInputError, SingularFactorError
 
 DENSE_SIZE_CAP = 20_000
 
 
-@dataclass(frozen=True)
-class RandomSource:
-    """`linalg.py:21-30`: PCG64 over SeedSequence(seed, spawn_key=(stream,))."""
-
-    seed: int
-    stream: int = 0
-
-    def generator(self) -> np.random.Generator:
-        ss = np.random.SeedSequence(entropy=self.seed, spawn_key=(self.stream,))
-        return np.random.Generator(np.random.PCG64(ss))
-
-
-@dataclass(frozen=True)
-class PivotedQR:
-    """`linalg.py:33-46`."""
-
-    q_factor: np.ndarray
-    r_factor: np.ndarray
-    kept: np.ndarray
-    dropped: np.ndarray
-    diag_ratios: np.ndarray
-
-
-def lattice_counts(count_per_dim: int, feature_count: int, dim: int, extra: int = 0) -> int:
-    """`assembly.py:32-40`: S * (integer ceil(K^(1/d)) + extra)."""
-    root = int(np.ceil(feature_count ** (1.0 / dim)))
-    while root > 1 and (root - 1) ** dim >= feature_count:
-        root -= 1
-    while root ** dim < feature_count:
-        root += 1
-    return count_per_dim * (root + extra)
+# featlsq's own value types (`linalg.py:21-46`) and lattice rule (`assembly.py:32-40`)
+RandomSource = ref_linalg.RandomSource
+PivotedQR = ref_linalg.PivotedQR
+lattice_counts = ref_assembly.lattice_counts
 
 
 def _check_matrix(a, name="matrix") -> np.ndarray:
@@ -69,21 +41,18 @@ def qr_column_pivot(a: np.ndarray, sigma_rel: float) -> PivotedQR:
     if cols == 0:
         e = np.empty(0, dtype=int)
         return PivotedQR(np.empty((rows, 0)), np.empty((0, 0)), e, e, np.empty(0))
+    from .filtering import factor_store
     from .solvers import _dense_blocks
-    t = D.torch()
     blocks = _dense_blocks(a)
-    dev = blocks.vals.device
-    R = t.empty(cols * cols, dtype=t.float64, device=dev)
-    perm = t.empty(cols, dtype=t.int32, device=dev)
-    rank = t.empty(1, dtype=t.int32, device=dev)
-    diag = t.empty(cols, dtype=t.float64, device=dev)
-    _lib.check(_lib.lib().fl_rrqr(C.byref(blocks.struct()), cols, max(rows, 1), float(sigma_rel),
-                                  D.ptr(R), D.ptr(perm), D.ptr(rank), D.ptr(diag),
-                                  D.stream_ptr()), "fl_rrqr")
+    # the same K2 as filter_system on a one-block store (route R for K >= 128)
+    work, R, perm, rank, diag = factor_store(blocks, float(sigma_rel))
+    blocks = D.DeviceBlocks(blocks.layout, work, blocks.ncols, blocks.col_off)
     r = int(D.to_host(rank)[0])
-    p = D.to_host(perm).astype(int)
+    if r < 0:
+        raise InvalidInputError("matrix contains non-finite entries")
+    p = D.to_host(perm)[:cols].astype(int)
     q = blocks.block_host(0, ncols=r) if r else np.zeros((rows, 0))
-    rr = D.to_host(R).reshape(cols, cols)[:r, :r].T.copy()
+    rr = D.to_host(R)[:cols * cols].reshape(cols, cols)[:r, :r].T.copy()
     return PivotedQR(q, rr, p[:r].copy(), np.sort(p[r:]), D.to_host(diag)[:r].copy())
 
 

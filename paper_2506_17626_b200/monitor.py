@@ -83,3 +83,12 @@ def test_error_fn(filtered, problem, dec, basis, test_set: TestSet) -> DeviceL1E
 
 
 test_error_fn.__test__ = False  # not a pytest test
+
+
+def raw_error_fn(problem, dec, basis, test_set: TestSet) -> DeviceL1Error:
+    """The runner's error function for solvers over the raw coefficients
+    (`runner.py:295-305`: l1_error(P a + lift)) with P on the device."""
+    return DeviceL1Error(None, SolutionBlocks(problem, dec, basis, test_set.points), test_set)
+
+
+raw_error_fn.__test__ = False

@@ -26,80 +26,38 @@ copied back at each recorded iteration to call it. Keyword-only `atol`/`btol`/`c
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
-from typing import Callable, Optional
+from dataclasses import dataclass
 
 import numpy as np
 
 from . import _device as D
 from . import _lib
+from ._featlsq import ref_assembly, ref_solvers
 from .errors import DivergenceError, InvalidInputError
 
 PROBE_CAP = 50_000_000  # entries of a host-callback operator probed onto the device
 
 
-class Operator:
-    """Minimal matvec/rmatvec wrapper (`solvers.py:24-30`)."""
-
-    def __init__(self, matvec, rmatvec, shape):
-        self.matvec = matvec
-        self.rmatvec = rmatvec
-        self.shape = shape
+Operator = ref_solvers.Operator                    # `solvers.py:24-30`
+ConvergenceMonitor = ref_solvers.ConvergenceMonitor  # `solvers.py:47-69`
 
 
-def as_operator(thing) -> Operator:
+def as_operator(thing):
     """`solvers.py:33-44`; products of device-backed inputs run on the device."""
     from .assembly import GlobalSystem, apply, apply_transpose
     if isinstance(thing, Operator):
         return thing
     if isinstance(thing, GlobalSystem):
         return Operator(lambda v: apply(thing, v), lambda r: apply_transpose(thing, r), thing.shape)
-    if hasattr(thing, "apply") and hasattr(thing, "apply_transpose"):
-        return Operator(thing.apply, thing.apply_transpose, thing.shape)
-    arr = np.asarray(thing, dtype=float)
-    if arr.ndim != 2:
-        raise InvalidInputError(f"cannot interpret {type(thing)} as an operator")
-    return Operator(lambda v: arr @ v, lambda r: arr.T @ r, arr.shape)
-
-
-@dataclass
-class ConvergenceMonitor:
-    """`solvers.py:47-69`: records (it, residual, error) every `stride`
-    iterations and keeps the lowest-error iterate."""
-
-    error_fn: Optional[Callable[[np.ndarray], float]] = None
-    stride: int = 1
-    records: list = field(default_factory=list)
-    best_error: float = np.inf
-    best_iteration: int = -1
-    best_iterate: np.ndarray | None = None
-
-    def observe(self, iteration: int, iterate: np.ndarray, residual_fn) -> None:
-        if self.stride > 1 and iteration % self.stride != 0:
-            return
-        residual = float(residual_fn())
-        error = float(self.error_fn(iterate)) if self.error_fn else residual
-        self.records.append((iteration, residual, error))
-        if error < self.best_error:
-            self.best_error = error
-            self.best_iteration = iteration
-            self.best_iterate = iterate.copy()
+    return ref_solvers.as_operator(thing)
 
 
 @dataclass(frozen=True)
-class SolveResult:
-    solution: np.ndarray
-    iterations_run: int
-    residual_norm: float
-    monitor: ConvergenceMonitor
-    breakdown: bool = False
-    istop: int = 0
+class SolveResult(ref_solvers.SolveResult):
+    """featlsq's `SolveResult` (`solvers.py:72-84`) plus scipy's `istop` code
+    when the keyword-only stopping rule is used (0 otherwise)."""
 
-    @property
-    def best_solution(self) -> np.ndarray:
-        if self.monitor.best_iterate is None:
-            return self.solution
-        return self.monitor.best_iterate
+    istop: int = 0
 
 
 def _dense_blocks(arr: np.ndarray) -> D.DeviceBlocks:
@@ -115,11 +73,12 @@ def _dense_blocks(arr: np.ndarray) -> D.DeviceBlocks:
 
 def device_operator(operator):
     """Resolve anything `as_operator` accepts to device blocks + shape."""
-    from .assembly import GlobalSystem
+    from .assembly import GlobalSystem, adopt_system
     from .filtering import PreconditionedOperator
     if isinstance(operator, PreconditionedOperator):
         return operator.device_blocks, operator.shape
-    if isinstance(operator, GlobalSystem):
+    if isinstance(operator, GlobalSystem) or isinstance(operator, ref_assembly.GlobalSystem):
+        operator = adopt_system(operator)
         operator.sync_device()
         return operator.store, operator.shape
     if isinstance(operator, D.DeviceBlocks):
@@ -357,7 +316,9 @@ def as_preconditioner(system, cutoff: float = 1e-14) -> AdditiveSchwarz:
     """`solvers.py:181-192` on the device: Gramians A_j^T A_j from the
     resident blocks (cuBLAS batched GEMM), eigendecomposition (cuSOLVER),
     eigenvalues at or below cutoff * largest dropped."""
+    from .assembly import adopt_system
     t = D.torch()
+    system = adopt_system(system)
     system.sync_device()
     st = system.store
     L = st.layout

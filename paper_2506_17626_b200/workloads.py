@@ -1,7 +1,7 @@
 """Synthetic BASELINE workloads (BASELINE.json `configs`).
 
 Each config becomes (ProblemSpec, Decomposition, FeatureBasis,
-interior_per_dim, sigma) built only from the public value types, so the same
+interior_per_dim, sigma) built from featlsq's own value types, so the same
 objects feed the device path and the CPU oracle. Weights are
 W ~ U(-w, w) of shape (J, M, d) and b ~ U(-1, 1) of shape (J, M), drawn from
 np.random.default_rng(seed); interior lattices are linspace with endpoints
@@ -19,9 +19,12 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .basis import FeatureBasis
-from .domains import Domain, decompose
-from .problems import ConstraintRows, LinearOperator2, ProblemSpec
+from ._featlsq import featlsq
+
+FeatureBasis = featlsq.FeatureBasis
+Domain, decompose = featlsq.Domain, featlsq.decompose
+ConstraintRows, LinearOperator2, ProblemSpec = (featlsq.ConstraintRows, featlsq.LinearOperator2,
+                                                featlsq.ProblemSpec)
 
 PI = np.pi
 

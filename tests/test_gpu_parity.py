@@ -254,22 +254,55 @@ def test_qr_edge_cases(fl):
     assert fl.qr_column_pivot(dup, 1e-8).kept.size == 5
 
 
-@pytest.mark.parametrize("K", [160, 192, 256, 704])
+@pytest.mark.parametrize("K", [160, 192, 224, 256, 704])
 def test_qr_column_pivot_both_routes_match_scipy(fl, K):
-    """K = 160 / 192 / 256 take route R (blocked: 32-wide updates for K = 160,
-    64-wide and the fused K2c for 192 / 256), K = 704 exceeds its
-    shared-memory bound and takes the direct kernel: all reproduce LAPACK's
-    kept sequence on a gapped-spectrum matrix (linalg.py:58-97)."""
+    """K = 160 / 224 take route R with the 32-wide branches (K2a panel +
+    wy_apply<32> loop, the 32-wide K2c loop), K = 192 / 256 the 64-wide
+    updates and the fused K2c; K = 704 exceeds route R's shared-memory bound
+    and takes the direct kernel (filtering.rrqr_route, the same selection
+    filter_system makes). All reproduce LAPACK's kept sequence on a
+    gapped-spectrum matrix, R norm-wise and Q's own gates (linalg.py:58-97)."""
+    from paper_2506_17626_b200 import _device as D
+    from paper_2506_17626_b200.filtering import rrqr_route
     rng = np.random.default_rng(K)
     m = 900
     u, _ = np.linalg.qr(rng.standard_normal((m, K)))
     w, _ = np.linalg.qr(rng.standard_normal((K, K)))
     s = np.logspace(0, -14, K)
     a = (u * s) @ w.T
+    route = rrqr_route(D.BlockLayout(m, K, [np.arange(m)]))
+    assert route == ("direct" if K > 640 else "blocked")
     _, r_ref, kept_ref, _, _ = O.qr_column_pivot(a, 1e-10)
     got = fl.qr_column_pivot(a, 1e-10)
     assert np.array_equal(got.kept, kept_ref)
     assert np.linalg.norm(got.r_factor - r_ref) <= 1e-10 * np.linalg.norm(r_ref)
+    q, r = got.q_factor, got.r_factor
+    assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-12
+    assert np.abs(q @ r - a[:, got.kept]).max() <= 1e-12 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("K", [160, 256])
+def test_route_r_rejects_non_finite(fl, K):
+    """Route R flags a block holding NaN or Inf with rank -1 (the finiteness
+    test of linalg.py:49-55); qr_column_pivot and filter_system raise
+    InvalidInputError like the reference (filtering.py:100 -> linalg.py:66)."""
+    from paper_2506_17626_b200 import workloads
+    rng = np.random.default_rng(1)
+    for bad in (np.nan, np.inf):
+        a = rng.standard_normal((400, K))
+        a[123, K // 2] = bad
+        with pytest.raises(fl.InvalidInputError, match="non-finite"):
+            fl.qr_column_pivot(a, 1e-10)
+    from paper_2506_17626_b200.filtering import rrqr_route
+    wl = workloads.build_small("cfg2" if K == 160 else "cfg3", M=K)
+    sysd = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    assert rrqr_route(sysd.store.layout) == "blocked"
+    blk = sysd.blocks[7]
+    mat = blk.matrix.copy()
+    mat[3, 5] = np.nan
+    sysd.blocks[7] = fl.SubdomainBlock(blk.subdomain, blk.rows, blk.columns, mat)
+    with pytest.raises(fl.InvalidInputError, match="non-finite"):
+        fl.filter_system(sysd, wl.sigma)
 
 
 # ---------------------------------------------------------------- LSQR unit cases

@@ -14,9 +14,9 @@ import pytest
 
 from oracle import featlsq_oracle as O
 from paper_2506_17626_b200 import workloads
-from paper_2506_17626_b200.basis import init_basis
-from paper_2506_17626_b200.domains import decompose
-from paper_2506_17626_b200.problems import oscillator_problem
+from featlsq.basis import init_basis
+from featlsq.domains import decompose
+from featlsq.problems import oscillator_problem
 
 CFGS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
 

@@ -14,9 +14,9 @@ import numpy as np
 import pytest
 
 from oracle import featlsq_oracle as O
-from paper_2506_17626_b200.basis import init_basis
-from paper_2506_17626_b200.domains import decompose
-from paper_2506_17626_b200.problems import laplace_problem, wave_problem
+from featlsq.basis import init_basis
+from featlsq.domains import decompose
+from featlsq.problems import laplace_problem, wave_problem
 
 CASES = {"laplace": (lambda: laplace_problem(3), 16, 2.9, 16),
          "wave": (lambda: wave_problem(0.4), 4, 2.9, 8)}
@@ -86,7 +86,7 @@ ACT_CASES = {"osc_sin": ("osc", "sin"), "osc_sigmoid": ("osc", "sigmoid"),
 
 
 def activation_case(name):
-    from paper_2506_17626_b200.problems import oscillator_problem
+    from featlsq.problems import oscillator_problem
     kind, act = ACT_CASES[name]
     if kind == "osc":
         p, S, K = oscillator_problem(60.0), 20, 8
