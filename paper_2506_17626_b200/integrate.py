@@ -39,6 +39,8 @@ _NAMES = {
     "lsqr": ("solvers", "runner"),                       # solvers.py:87
     "cg_normal": ("solvers", "runner"),                  # solvers.py:195
     "as_preconditioner": ("solvers", "runner"),          # solvers.py:178
+    "as_operator": ("solvers", "runner"),                # solvers.py:33
+    "AdditiveSchwarz": ("solvers",),                     # solvers.py:149 (device block products)
 }
 
 

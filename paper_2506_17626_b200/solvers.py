@@ -43,13 +43,24 @@ ConvergenceMonitor = ref_solvers.ConvergenceMonitor  # `solvers.py:47-69`
 
 
 def as_operator(thing):
-    """`solvers.py:33-44`; products of device-backed inputs run on the device."""
-    from .assembly import GlobalSystem, apply, apply_transpose
+    """`solvers.py:33-44`, with a `GlobalSystem` (device-resident or featlsq's
+    host one) applied through the device block products."""
+    from .assembly import GlobalSystem, adopt_system, apply, apply_transpose
     if isinstance(thing, Operator):
         return thing
-    if isinstance(thing, GlobalSystem):
-        return Operator(lambda v: apply(thing, v), lambda r: apply_transpose(thing, r), thing.shape)
-    return ref_solvers.as_operator(thing)
+    if isinstance(thing, (GlobalSystem, ref_assembly.GlobalSystem)):
+        system = adopt_system(thing)
+        return Operator(lambda v: apply(system, v), lambda r: apply_transpose(system, r),
+                        system.shape)
+    if hasattr(thing, "apply") and hasattr(thing, "apply_transpose"):
+        return Operator(thing.apply, thing.apply_transpose, thing.shape)
+    try:
+        arr = np.asarray(thing, dtype=float)
+    except (TypeError, ValueError):
+        arr = np.zeros(0)
+    if arr.ndim != 2:
+        raise InvalidInputError(f"cannot interpret {type(thing)} as an operator")
+    return Operator(lambda v: arr @ v, lambda r: arr.T @ r, arr.shape)
 
 
 @dataclass(frozen=True)
@@ -388,6 +399,11 @@ def cg_normal(operator, rhs: np.ndarray, max_iters: int,
     state = t.from_numpy(np.frombuffer(bytes(sst), dtype=np.uint8).copy()).to(dev)
     L = _lib.lib()
     op = C.byref(blocks.struct())
+    if preconditioner is not None and not isinstance(preconditioner, AdditiveSchwarz):
+        # featlsq's own AdditiveSchwarz (solvers.py:149-175): same fields
+        preconditioner = AdditiveSchwarz(preconditioner.column_count, preconditioner.block_ranges,
+                                         preconditioner.block_inverses,
+                                         preconditioner.degenerate_blocks)
     pre = C.byref(preconditioner.device_struct()) if preconditioner is not None else None
     _lib.check(L.fl_cg_init(op, C.byref(vecs), pre, D.ptr(state), D.stream_ptr()), "fl_cg_init")
     err_trace = None

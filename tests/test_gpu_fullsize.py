@@ -25,7 +25,7 @@
 4. cfg3 against the REFERENCE's own end-to-end run (tests/golden/
    lsqr_full_cfg3.npz: featlsq assemble -> filter_system -> lsqr 10 000 ->
    recover_solution, tests/golden/make_golden_lsqr_full.py): runs L and D
-   within the same bound as in 3, phibar to 1e-6.
+   within the same bound as in 3.
 """
 
 from __future__ import annotations
@@ -200,9 +200,11 @@ def test_full_size_solution_within_own_spread(fl, full, golden_dir):
           + f" | l1 D {fd[3]:.6e} L {fl_[3]:.6e} D' {fp[3]:.6e}")
     for n in names:
         assert dl[n] <= max(1e-8, 10.0 * dp[n]), n
-    assert dl["Ma"] <= 1e-6 and dl["pred"] <= 1e-5
-    assert abs(ph_d - ph_l) <= 1e-6 * ph_l
-    assert abs(fd[3] - fl_[3]) <= 1e-5 * fl_[3]
+    # the spread itself stays small (the gate above is not vacuous)
+    assert dp["Ma"] <= 1e-5 and dp["pred"] <= 1e-4
+    sp_ph = abs(ph_p - ph_d)
+    assert abs(ph_d - ph_l) <= max(1e-9 * ph_l, 10.0 * sp_ph)
+    assert abs(fd[3] - fl_[3]) <= max(1e-9 * fl_[3], 10.0 * abs(fp[3] - fd[3]))
     del fs_p, pert
     path = os.path.join(golden_dir, f"lsqr_full_{name}.npz")
     if not os.path.exists(path):
@@ -220,7 +222,7 @@ def test_full_size_solution_within_own_spread(fl, full, golden_dir):
     for n in names:
         assert rl[n] <= max(1e-8, 10.0 * dp[n]), n
         assert rd[n] <= max(1e-8, 10.0 * dp[n]), n
-    assert abs(ph_d - float(g["residual"])) <= 1e-6 * float(g["residual"])
+    assert abs(ph_d - float(g["residual"])) <= max(1e-9 * ph_d, 10.0 * sp_ph)
 
 
 def test_full_size_lsqr_properties(fl, full):
