@@ -119,7 +119,7 @@ typedef struct fl_assembly_desc {
   const int64_t* con_ptr;   /* (J+1,) */
   const int32_t* con_idx;   /* constraint point index */
   const int32_t* con_grp;   /* constraint group */
-  int32_t n_tiles;          /* row tiles of FL_ASM_TILE rows */
+  int32_t n_tiles;          /* row tiles of fl_assemble_tile_rows() rows */
   const int32_t* tiles;     /* (n_tiles, 2): block, first row */
   /* hard-constraint mask (assembly.py:107-114): the window jet along axis a
      is multiplied by the mask's jet along a, given per point as (value,
@@ -130,7 +130,10 @@ typedef struct fl_assembly_desc {
                                lattice point = sum_i index_i * stride_i) */
 } fl_assembly_desc;
 
-#define FL_ASM_TILE 256
+/* rows per K1 tile: the `tiles` table lists (block, first row) in steps of
+   fl_assemble_tile_rows() rows (FL_ASM_TILE in this build) */
+#define FL_ASM_TILE 512
+int32_t fl_assemble_tile_rows(void);
 
 int fl_assemble(const fl_assembly_desc* desc, const fl_blockop* out, void* stream);
 

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("FEATLSQ_LIB") or os.path.join(HERE, "libfeatlsq_b200.
 
 FL_OK, FL_ERR_INVALID, FL_ERR_DEGENERATE, FL_ERR_DIVERGENCE, FL_ERR_SINGULAR, FL_ERR_CUDA = \
     0, -1, -2, -3, -4, -5
-FL_ROW_TILE, FL_COL_TILE, FL_ASM_TILE = 256, 32, 256
+FL_ROW_TILE, FL_COL_TILE = 256, 32
 FL_LSQR_SPLIT_MAX = 4
 FL_TBUILD_ROWS = 16
 
@@ -135,6 +135,8 @@ def lib():
     L.fl_version.argtypes = []
     L.fl_last_error.restype = C.c_char_p
     L.fl_last_error.argtypes = []
+    L.fl_assemble_tile_rows.restype = C.c_int32
+    L.fl_assemble_tile_rows.argtypes = []
     L.fl_rrqr_blocked_workspace.restype = C.c_int64
     L.fl_rrqr_blocked_workspace.argtypes = [C.c_int32, C.c_int32, C.c_int64]
     _lib = L
@@ -146,7 +148,7 @@ EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", 
             "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error",
             "fl_error_blocks", "fl_monitor_error", "fl_lsqr_iterate_monitored",
             "fl_lsqr_monitor_flush", "fl_cg_init", "fl_cg_iterate", "fl_cg_residual",
-            "fl_block_precond_apply", "fl_probe_read")
+            "fl_block_precond_apply", "fl_probe_read", "fl_assemble_tile_rows")
 
 
 def check(code: int, what: str) -> None:

@@ -1,7 +1,7 @@
 // K1 — fused block assembly (reference: featlsq assembly.py:124-238).
 //
-// One CTA per (block j, tile of FL_ASM_TILE = 256 rows), one row per thread;
-// see assemble_kernel below for the two phases. Padding rows [m_j, ld_j)
+// One CTA per (block j, tile of FL_ASM_TILE = 512 rows), two adjacent rows
+// per thread; see assemble_kernel below for the two phases. Padding rows [m_j, ld_j)
 // are written as exact zeros.
 //
 // Roofline: HBM write of 8 B per entry; the FP64 work per entry is one
@@ -11,8 +11,7 @@
 
 namespace {
 
-constexpr int NT = FL_ASM_TILE;
-static_assert(NT == 256, "one row per thread");
+constexpr int NT = 256;
 constexpr int MAXD = 3;
 
 struct Jet {
@@ -56,7 +55,21 @@ __device__ __forceinline__ Jet raw_factor(double t, double mu, double half) {
 
 // tanh for |error| <= a few ulp of 1 (absolute): 1 - 2 / (exp(2x) + 1).
 // exp overflow gives rcp(inf) = 0 -> 1, underflow gives -1: no clamping.
-__device__ __forceinline__ double tanh_fast(double x) { return 1.0 - 2.0 * __drcp_rn(exp(2.0 * x) + 1.0); }
+// 1 / d for d in [1, 1e300]: MUFU approximation + two Newton steps (the
+// relative error squares per step: full precision, <= 1 ulp; no special-case
+// branches, which __drcp_rn carries)
+__device__ __forceinline__ double rcp_newton(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+// tanh(x) = 1 - 2 / (E + 1), E = exp(2x) <= 1e300 (E = 0 gives -1)
+__device__ __forceinline__ double tanh_from_exp2x(double E) { return fma(-2.0, rcp_newton(E + 1.0), 1.0); }
+// general argument: exp(2x) clamped below overflow (tanh is 1.0 in fp64 far before)
+__device__ __forceinline__ double tanh_fast(double x) { return tanh_from_exp2x(fmin(exp(2.0 * x), 1e300)); }
 
 // activation value and its first two derivatives at pre (basis.py:119-126)
 __device__ __forceinline__ void activation(int act, double pre, double& tv, double& g1, double& g2) {
@@ -78,43 +91,142 @@ __device__ __forceinline__ void activation(int act, double pre, double& tv, doub
   }
 }
 
-constexpr int CK = 32;        // columns per chunk
-constexpr int TLMAX = 192;    // lattice coordinates per chunk table (sum over axes)
-constexpr double EXP_SAFE = 300.0;  // |2 (x~ W + b)| bound of one table factor
+#ifndef ASM_MINB
+#define ASM_MINB 3
+#endif
+constexpr int CK = 64;        // columns per chunk
+constexpr int TLMAX = 96;     // lattice coordinates per chunk table (sum over axes)
+#ifndef ASM_RPT
+#define ASM_RPT 2
+#endif
+constexpr int RPT = ASM_RPT;  // adjacent rows per thread (16-byte stores)
+static_assert(RPT % 2 == 0, "rows are stored in pairs");
+constexpr int TILE = NT * RPT;
+// |2 (x~ W + b)| bound of one table factor: a product of D <= 3 factors
+// stays below exp(690) < DBL_MAX, so E + 1 needs no clamp on the table path
+constexpr double EXP_SAFE = 230.0;
 
-// One CTA per (block j, tile of NT rows), one row per thread.
-//
-// Phase 1 (per row): the point, the normalised partition-of-unity window
+// Per-row coefficients of entry(r, k) = t A + g1 sum_a fp_ka B_a + g2 sum_a fp_ka^2 C_a.
+struct RowCoef {
+  double A, B[MAXD], C[MAXD], xt[MAXD];
+  int tix[MAXD];
+  bool valid, on_box;
+};
+
+// Phase 1 for one row: the point, the normalised partition-of-unity window
 // jets along every axis (domains.py:109-173: raw (1+cos)^2 factors,
 // normaliser over the covering centers in index order, jet quotient
 // jets.py:76-80, products jets.py:55-63, mask jets assembly.py:111-112),
 // folded with the operator coefficients (problems.py:39-47) and the row
-// weight (assembly.py:180-190) into
-//   entry(r, k) = t A_r + g1 sum_a fp_ka B_ra + g2 sum_a fp_ka^2 C_ra
+// weight (assembly.py:180-190).
+template <int D>
+__device__ __forceinline__ void row_coef(const fl_assembly_desc& d, int j, int r, int m, int boxcount,
+                                         const int32_t* box, const int (&sidx)[MAXD], const double (*scoef)[2 + 2 * MAXD],
+                                         RowCoef& rc) {
+  const int S = d.count_per_dim;
+  rc.A = 0.0;
+  rc.valid = r < m;
+  rc.on_box = false;
+#pragma unroll
+  for (int a = 0; a < MAXD; ++a) {
+    rc.B[a] = rc.C[a] = rc.xt[a] = 0.0;
+    rc.tix[a] = 0;
+  }
+  if (!rc.valid) return;
+  double x[MAXD];
+  const double* mk = nullptr;  // mask jets of this point, (D, 3)
+  int coef = 0;
+  if (r < boxcount) {
+    int rem = r;
+    int64_t gid = 0;
+    for (int i = D - 1; i >= 0; --i) {
+      const int n = box[2 * i + 1];
+      const int digit = rem % n;
+      rem /= n;
+      x[i] = d.axes[d.axis_off[i] + box[2 * i] + digit];
+      gid += (int64_t)(box[2 * i] + digit) * d.lattice_stride[i];
+      rc.tix[i] = digit;
+    }
+    rc.on_box = true;
+    if (d.mask_int) mk = d.mask_int + gid * D * 3;
+  } else {
+    const int64_t e = d.con_ptr[j] + (r - boxcount);
+    const int pi = d.con_idx[e];
+    for (int i = 0; i < D; ++i) x[i] = d.con_pts[(int64_t)pi * D + i];
+    coef = 1 + d.con_grp[e];
+    if (d.mask_con) mk = d.mask_con + (int64_t)pi * D * 3;
+  }
+  double fval[MAXD];
+  Jet ffull[MAXD];
+  for (int i = 0; i < D; ++i) {
+    const double* cen = d.centers + (int64_t)i * S;
+    const double half = d.half[i];
+    const double t = x[i];
+    Jet num = raw_factor(t, cen[sidx[i]], half);
+    Jet den{0.0, 0.0, 0.0};
+    int l = sidx[i] - d.reach, h = sidx[i] + d.reach;
+    if (l < 0) l = 0;
+    if (h > S - 1) h = S - 1;
+    for (int s2 = l; s2 <= h; ++s2) {  // non-covering centers add exact zeros
+      Jet f = raw_factor(t, cen[s2], half);
+      den.v += f.v;
+      den.f += f.f;
+      den.s += f.s;
+    }
+    ffull[i] = jmul(num, jrecip(den));
+    Jet numv{num.v, 0.0, 0.0}, denv{den.v, 0.0, 0.0};
+    fval[i] = jmul(numv, jrecip(denv)).v;
+    rc.xt[i] = (t - cen[sidx[i]]) / half;
+  }
+  const double* co = scoef[coef];
+  const double weight = co[1];
+  double wv = 0.0, acc = 0.0;
+  for (int a = 0; a < D; ++a) {
+    Jet w{0.0, 0.0, 0.0};
+    for (int i = 0; i < D; ++i) {
+      Jet fi = (i == a) ? ffull[i] : Jet{fval[i], 0.0, 0.0};
+      w = (i == 0) ? fi : jmul(w, fi);
+    }
+    if (mk) w = jmul(w, Jet{mk[3 * a], mk[3 * a + 1], mk[3 * a + 2]});
+    if (a == 0) {
+      wv = w.v;
+      acc = co[0] * wv;
+    }
+    const double c1 = co[2 + a], c2 = co[2 + D + a];
+    acc += c1 * w.f + c2 * w.s;
+    rc.B[a] = weight * (c1 * wv + 2.0 * c2 * w.f);
+    rc.C[a] = weight * (c2 * wv);
+  }
+  rc.A = weight * acc;
+}
+
+// One CTA per (block j, tile of NT * RPT rows); thread t owns rows RPT t ..
+// RPT t + RPT - 1 of the tile and writes them with 16-byte stores.
+//
+// Phase 1 (row_coef above) folds everything that depends only on the row
+// into entry(r, k) = t A_r + g1 sum_a fp_ka B_ra + g2 sum_a fp_ka^2 C_ra,
 // with t, g1, g2 the activation jet of feature k at row r and fp_ka =
 // W_ka / h_a (basis.py:119-126; the product rule of assembly.py:107-114
 // regrouped by activation derivative).
 //
-// Phase 2 (per 32-column chunk): tanh features on an interior lattice box
+// Phase 2 (per 64-column chunk): tanh features on an interior lattice box
 // use exp(2 (x~ . W_k + b_k)) = prod_a exp(2 (x~_a W_ka [+ b_k])): the
 // per-axis factors of the lattice coordinates the tile touches are
-// tabulated once per chunk (a few hundred exps for 8192 entries), so an
-// entry costs D - 1 multiplies, one reciprocal and ~12 FMAs; rows off the
-// lattice (constraint points), other activations and blocks whose factors
-// could overflow evaluate exp / sincos per entry. Stores are column-major:
-// a warp writes 32 consecutive rows of one column (256 B).
+// tabulated once per chunk (~60 exps for 16384 entries), so an entry costs
+// D - 1 multiplies, one reciprocal (MUFU + 2 Newton steps) and ~10 FMAs,
+// with the column terms fp, fp^2 shared by the thread's two rows; rows off
+// the lattice (constraint points), other activations and blocks whose
+// factors could overflow evaluate exp / sincos per entry.
 template <int D>
-__global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double* __restrict__ vals,
-                                                      const int64_t* __restrict__ boff,
-                                                      const int32_t* __restrict__ bld,
-                                                      const int32_t* __restrict__ bm) {
+__global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble_kernel(fl_assembly_desc d, double* __restrict__ vals,
+                                                         const int64_t* __restrict__ boff,
+                                                         const int32_t* __restrict__ bld,
+                                                         const int32_t* __restrict__ bm) {
   extern __shared__ double smem[];
   const int K = d.nfeat;
-  double* tab = smem;            // (CK, TLMAX) exp table of one column chunk
-  double* sW = tab + CK * TLMAX; // (K, D)
-  double* sB = sW + K * D;       // (K)
-  double* sF1 = sB + K;          // (K, D) W / h
-  double* sF2 = sF1 + K * D;     // (K, D) (W / h)^2
+  double* tab = smem;             // (CK, TLMAX) exp table of one column chunk
+  double* sW = tab + CK * TLMAX;  // (K, D)
+  double* sB = sW + K * D;        // (K)
   __shared__ double scoef[8][2 + 2 * MAXD];
 
   const int j = d.tiles[2 * blockIdx.x];
@@ -127,10 +239,7 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
   for (int i = threadIdx.x; i < K * D; i += NT) {
     const int a = i % D;
     const double w = d.weights[(int64_t)j * K * D + i];
-    const double fp = w * (1.0 / d.half[a]);
     sW[i] = w;
-    sF1[i] = fp;
-    sF2[i] = fp * fp;
     double e = fabs(2.0 * w);
     if (a == 0) e += fabs(2.0 * d.biases[(int64_t)j * K + i / D]);
     unsafe |= !(e <= EXP_SAFE);
@@ -156,12 +265,12 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
   for (int i = 0; i < D; ++i) boxcount *= box[2 * i + 1];
 
   // lattice-coordinate ranges of this tile's box rows, per axis
-  int lo[MAXD], cnt[MAXD], base[MAXD];
+  int lo[MAXD] = {0, 0, 0}, base[MAXD] = {0, 0, 0};
   int tl = 0;
-  const int rb1 = min(r0 + NT, min(boxcount, m));
+  const int rb1 = min(r0 + TILE, min(boxcount, m));
   bool use_tab = (d.activation == FL_ACT_TANH) && D >= 2 && rb1 > r0;
   if (use_tab) {
-    int st = 1;
+    int st = 1, cnt[MAXD];
     for (int a = D - 1; a >= 0; --a) {
       const int n = box[2 * a + 1];
       const int q0 = r0 / st, q1 = (rb1 - 1) / st;
@@ -184,151 +293,136 @@ __global__ void __launch_bounds__(NT) assemble_kernel(fl_assembly_desc d, double
     use_tab = tl <= TLMAX;
   }
 
-  // ---- phase 1: this thread's row ----
-  const int r = r0 + threadIdx.x;
-  bool valid = r < m, on_box = false;
-  double A = 0.0, Bc[MAXD], Cc[MAXD], xt[MAXD];
-  int tix[MAXD];
-  for (int a = 0; a < MAXD; ++a) {
-    Bc[a] = Cc[a] = xt[a] = 0.0;
-    tix[a] = 0;
-  }
-  if (valid) {
-    double x[MAXD];
-    const double* mk = nullptr;  // mask jets of this point, (D, 3)
-    int coef = 0;
-    if (r < boxcount) {
-      int rem = r;
-      int64_t gid = 0;
-      for (int i = D - 1; i >= 0; --i) {
-        const int n = box[2 * i + 1];
-        const int digit = rem % n;
-        rem /= n;
-        x[i] = d.axes[d.axis_off[i] + box[2 * i] + digit];
-        gid += (int64_t)(box[2 * i] + digit) * d.lattice_stride[i];
-        tix[i] = digit;
-      }
-      on_box = true;
-      if (d.mask_int) mk = d.mask_int + gid * D * 3;
-    } else {
-      const int64_t e = d.con_ptr[j] + (r - boxcount);
-      const int pi = d.con_idx[e];
-      for (int i = 0; i < D; ++i) x[i] = d.con_pts[(int64_t)pi * D + i];
-      coef = 1 + d.con_grp[e];
-      if (d.mask_con) mk = d.mask_con + (int64_t)pi * D * 3;
-    }
-    // per-dim normalised factors: value-only and full jets
-    double fval[MAXD];
-    Jet ffull[MAXD];
-    for (int i = 0; i < D; ++i) {
-      const double* cen = d.centers + (int64_t)i * S;
-      const double half = d.half[i];
-      const double t = x[i];
-      Jet num = raw_factor(t, cen[sidx[i]], half);
-      Jet den{0.0, 0.0, 0.0};
-      int l = sidx[i] - d.reach, h = sidx[i] + d.reach;
-      if (l < 0) l = 0;
-      if (h > S - 1) h = S - 1;
-      for (int s2 = l; s2 <= h; ++s2) {  // non-covering centers add exact zeros
-        Jet f = raw_factor(t, cen[s2], half);
-        den.v += f.v;
-        den.f += f.f;
-        den.s += f.s;
-      }
-      ffull[i] = jmul(num, jrecip(den));
-      Jet numv{num.v, 0.0, 0.0}, denv{den.v, 0.0, 0.0};
-      fval[i] = jmul(numv, jrecip(denv)).v;
-      xt[i] = (t - cen[sidx[i]]) / half;
-    }
-    const double* co = scoef[coef];
-    const double weight = co[1];
-    double wv = 0.0;
-    double acc = 0.0;
-    for (int a = 0; a < D; ++a) {
-      Jet w{0.0, 0.0, 0.0};
-      for (int i = 0; i < D; ++i) {
-        Jet fi = (i == a) ? ffull[i] : Jet{fval[i], 0.0, 0.0};
-        w = (i == 0) ? fi : jmul(w, fi);
-      }
-      if (mk) w = jmul(w, Jet{mk[3 * a], mk[3 * a + 1], mk[3 * a + 2]});
-      if (a == 0) {
-        wv = w.v;
-        acc = co[0] * wv;
-      }
-      const double c1 = co[2 + a], c2 = co[2 + D + a];
-      acc += c1 * w.f + c2 * w.s;
-      Bc[a] = weight * (c1 * wv + 2.0 * c2 * w.f);
-      Cc[a] = weight * (c2 * wv);
-    }
-    A = weight * acc;
-  }
+  // ---- phase 1: this thread's two rows ----
+  const int rA = r0 + RPT * threadIdx.x;
+  RowCoef rc[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) row_coef<D>(d, j, rA + u, m, boxcount, box, sidx, scoef, rc[u]);
   unsafe = __syncthreads_or(unsafe);
   use_tab = use_tab && !unsafe;
-  const bool store = r < ld;  // rows past the padding only help build the tables
-  double* out = vals + boff[j] + r;
-  int toff[MAXD];
-  for (int a = 0; a < D; ++a) toff[a] = base[a] + tix[a] - lo[a];
-  const bool row_tab = use_tab && on_box;
+  // ld is a multiple of 16: all RPT rows are stored or none
+  const bool store = rA < ld;
+  double* out = vals + boff[j] + rA;
+  bool row_tab = use_tab;
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) row_tab = row_tab && (rc[u].on_box || (u > 0 && !rc[u].valid));
+  int toff[RPT][MAXD];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u)
+#pragma unroll
+    for (int a = 0; a < MAXD; ++a) toff[u][a] = a < D ? base[a] + rc[u].tix[a] - lo[a] : 0;
+  double invh[MAXD];
+#pragma unroll
+  for (int a = 0; a < MAXD; ++a) invh[a] = a < D ? 1.0 / d.half[a] : 0.0;
 
-  // ---- phase 2: 32-column chunks ----
+  // column terms fp_a, fp_a^2 of feature k (shared by the two rows)
+  auto col_terms = [&](int k, double (&f1)[MAXD], double (&f2)[MAXD]) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      f1[a] = sW[k * D + a] * invh[a];
+      f2[a] = f1[a] * f1[a];
+    }
+  };
+  auto entry = [&](const RowCoef& c, const double (&f1)[MAXD], const double (&f2)[MAXD], double tv, double g1,
+                   double g2) {
+    double p1 = f1[0] * c.B[0], p2 = f2[0] * c.C[0];
+#pragma unroll
+    for (int a = 1; a < D; ++a) {
+      p1 += f1[a] * c.B[a];
+      p2 += f2[a] * c.C[a];
+    }
+    return tv * c.A + g1 * p1 + g2 * p2;
+  };
+  // tanh: g2 = -2 t g1, so entry = t A + g1 (p1 - 2 t p2)
+  auto entry_tanh = [&](const RowCoef& c, const double (&f1)[MAXD], const double (&f2)[MAXD], double tv) {
+    double p1 = f1[0] * c.B[0], p2 = f2[0] * c.C[0];
+#pragma unroll
+    for (int a = 1; a < D; ++a) {
+      p1 += f1[a] * c.B[a];
+      p2 += f2[a] * c.C[a];
+    }
+    const double g1 = fma(-tv, tv, 1.0);
+    return fma(g1, fma(-2.0 * tv, p2, p1), tv * c.A);
+  };
+
+  // this thread's table coordinate: q = tid mod tl (axis ta, normalised
+  // coordinate txa), columns tc, tc + tcs, ... of every chunk
+  const int tcs = use_tab ? NT / tl : 1;
+  const int tq = use_tab ? threadIdx.x % tl : 0, tc = use_tab ? threadIdx.x / tl : 0;
+  int ta = 0;
+  double txa = 0.0;
+  if (use_tab && tc < tcs) {
+    while (ta + 1 < D && tq >= base[ta + 1]) ++ta;
+    const int digit = lo[ta] + (tq - base[ta]);
+    txa = (d.axes[d.axis_off[ta] + box[2 * ta] + digit] - d.centers[(int64_t)ta * S + sidx[ta]]) * invh[ta];
+  }
+
+  // ---- phase 2: 64-column chunks ----
   for (int k0 = 0; k0 < K; k0 += CK) {
     const int nk = min(CK, K - k0);
     if (use_tab) {
       __syncthreads();
-      // tab[c * TLMAX + base_a + i] = exp(2 (x~_a(i) W_{k0+c, a} [+ b]))
-      for (int p = threadIdx.x; p < nk * tl; p += NT) {
-        const int c = p / tl, q = p % tl;
-        int a = 0;
-        while (a + 1 < D && q >= base[a + 1]) ++a;
-        const int digit = lo[a] + (q - base[a]);
-        const double xa = (d.axes[d.axis_off[a] + box[2 * a] + digit] - d.centers[(int64_t)a * S + sidx[a]]) /
-                          d.half[a];
-        double e = xa * sW[(k0 + c) * D + a];
-        if (a == 0) e += sB[k0 + c];
-        tab[c * TLMAX + q] = exp(2.0 * e);
-      }
+      // tab[c * TLMAX + q] = exp(2 (x~ W_{k0+c, a} [+ b_{k0+c}])), thread -> fixed q
+      if (tc < tcs)
+        for (int c = tc; c < nk; c += tcs) {
+          double e = txa * sW[(k0 + c) * D + ta];
+          if (ta == 0) e += sB[k0 + c];
+          tab[c * TLMAX + tq] = exp(2.0 * e);
+        }
       __syncthreads();
     }
     if (!store) continue;
-    if (!valid) {
-      for (int c = 0; c < nk; ++c) out[(int64_t)(k0 + c) * ld] = 0.0;
-      continue;
-    }
-    for (int c = 0; c < nk; ++c) {
-      const int k = k0 + c;
-      double tv, g1, g2;
-      if (row_tab) {
-        double E = tab[c * TLMAX + toff[0]];
+    if (row_tab) {
+#pragma unroll 2
+      for (int c = 0; c < nk; ++c) {
+        const int k = k0 + c;
+        double f1[MAXD], f2[MAXD];
+        col_terms(k, f1, f2);
+        double v[RPT];
 #pragma unroll
-        for (int a = 1; a < D; ++a) E *= tab[c * TLMAX + toff[a]];
-        tv = 1.0 - 2.0 * __drcp_rn(E + 1.0);
-        g1 = 1.0 - tv * tv;
-        g2 = -2.0 * tv * g1;
-      } else {
-        double pre = xt[0] * sW[k * D + 0];
+        for (int u = 0; u < RPT; ++u) {
+          double E = tab[c * TLMAX + toff[u][0]];
+          if (D > 1) E *= tab[c * TLMAX + toff[u][1]];
+          if (D > 2) E *= tab[c * TLMAX + toff[u][2]];
+          v[u] = rc[u].valid ? entry_tanh(rc[u], f1, f2, tanh_from_exp2x(E)) : 0.0;
+        }
 #pragma unroll
-        for (int i = 1; i < D; ++i) pre += xt[i] * sW[k * D + i];
-        pre += sB[k];
-        activation(d.activation, pre, tv, g1, g2);
+        for (int u = 0; u < RPT; u += 2)
+          *reinterpret_cast<double2*>(out + (int64_t)k * ld + u) = make_double2(v[u], v[u + 1]);
       }
-      double p1 = sF1[k * D] * Bc[0], p2 = sF2[k * D] * Cc[0];
+    } else {
+      for (int c = 0; c < nk; ++c) {
+        const int k = k0 + c;
+        double f1[MAXD], f2[MAXD];
+        col_terms(k, f1, f2);
+        double v[RPT];
 #pragma unroll
-      for (int a = 1; a < D; ++a) {
-        p1 += sF1[k * D + a] * Bc[a];
-        p2 += sF2[k * D + a] * Cc[a];
+        for (int u = 0; u < RPT; ++u) {
+          double pre = rc[u].xt[0] * sW[k * D + 0];
+#pragma unroll
+          for (int i = 1; i < D; ++i) pre += rc[u].xt[i] * sW[k * D + i];
+          pre += sB[k];
+          double tv, g1, g2;
+          activation(d.activation, pre, tv, g1, g2);
+          v[u] = rc[u].valid ? entry(rc[u], f1, f2, tv, g1, g2) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RPT; u += 2)
+          *reinterpret_cast<double2*>(out + (int64_t)k * ld + u) = make_double2(v[u], v[u + 1]);
       }
-      out[(int64_t)k * ld] = tv * A + g1 * p1 + g2 * p2;
     }
   }
 }
 
 }  // namespace
 
+extern "C" int32_t fl_assemble_tile_rows(void) { return TILE; }
+
 extern "C" int fl_assemble(const fl_assembly_desc* desc, const fl_blockop* out, void* stream) {
   if (desc->dim < 1 || desc->dim > MAXD || desc->ngroups > 7) return FL_ERR_INVALID;
   if (desc->n_tiles == 0) return FL_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  size_t smem = ((size_t)desc->nfeat * (3 * desc->dim + 1) + CK * TLMAX) * sizeof(double);
+  size_t smem = ((size_t)desc->nfeat * (desc->dim + 1) + CK * TLMAX) * sizeof(double);
   if (smem > 220 * 1024) return FL_ERR_INVALID;
   switch (desc->dim) {
     case 1:
