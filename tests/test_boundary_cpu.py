@@ -19,7 +19,7 @@ HEADER = os.path.join(ROOT, "include", "featlsq_b200.h")
 
 def _declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(fl_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(fl_\w+)\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
