@@ -284,6 +284,14 @@ typedef struct fl_block_precond {
   const double* vals;
 } fl_block_precond;
 
+/* Additive-Schwarz setup (solvers.py:178-192): per block j of A (ncols_j <=
+ * FL_AS_MAX_K) the Gramian A_j^T A_j, its Jacobi eigendecomposition and the
+ * pseudo-inverse over eigenvalues > cutoff * the largest, written row-major
+ * to inv + j * ncols_j^2 (a dense K x K per block: blocks of equal width);
+ * degenerate[j] = 1 when the cutoff dropped an eigenvalue. */
+#define FL_AS_MAX_K 96
+int fl_as_setup(const fl_blockop* A, double cutoff, double* inv, int32_t* degenerate, void* stream);
+
 /* z = P r on its own (AdditiveSchwarz.apply) */
 int fl_block_precond_apply(const fl_block_precond* pre, const double* r, double* z, void* stream);
 /* r = M^T rhs, z = P r, p = z, r.z (pre may be NULL) */

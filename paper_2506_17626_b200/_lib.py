@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("FEATLSQ_LIB") or os.path.join(HERE, "libfeatlsq_b200.
 FL_OK, FL_ERR_INVALID, FL_ERR_DEGENERATE, FL_ERR_DIVERGENCE, FL_ERR_SINGULAR, FL_ERR_CUDA = \
     0, -1, -2, -3, -4, -5
 FL_ROW_TILE, FL_COL_TILE = 256, 32
+FL_AS_MAX_K = 96
 FL_LSQR_SPLIT_MAX = 4
 FL_TBUILD_ROWS = 16
 
@@ -126,6 +127,7 @@ def lib():
                           C.c_int64, C.c_int64, C.POINTER(TestMonitor), vp],
         "fl_cg_residual": [C.POINTER(BlockOp), C.POINTER(CgVecs), vp, vp],
         "fl_block_precond_apply": [C.POINTER(BlockPrecond), vp, vp, vp],
+        "fl_as_setup": [C.POINTER(BlockOp), C.c_double, vp, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -148,7 +150,7 @@ EXPORTED = ("fl_assemble", "fl_rrqr", "fl_blockop_apply", "fl_blockop_apply_t", 
             "fl_rrqr_blocked", "fl_rrqr_blocked_workspace", "fl_version", "fl_last_error",
             "fl_error_blocks", "fl_monitor_error", "fl_lsqr_iterate_monitored",
             "fl_lsqr_monitor_flush", "fl_cg_init", "fl_cg_iterate", "fl_cg_residual",
-            "fl_block_precond_apply", "fl_probe_read", "fl_assemble_tile_rows")
+            "fl_block_precond_apply", "fl_probe_read", "fl_assemble_tile_rows", "fl_as_setup")
 
 
 def check(code: int, what: str) -> None:

@@ -53,8 +53,6 @@ __device__ __forceinline__ Jet raw_factor(double t, double mu, double half) {
   return r;
 }
 
-// tanh for |error| <= a few ulp of 1 (absolute): 1 - 2 / (exp(2x) + 1).
-// exp overflow gives rcp(inf) = 0 -> 1, underflow gives -1: no clamping.
 // 1 / d for d in [1, 1e300]: MUFU approximation + two Newton steps (the
 // relative error squares per step: full precision, <= 1 ulp; no special-case
 // branches, which __drcp_rn carries)
@@ -66,10 +64,11 @@ __device__ __forceinline__ double rcp_newton(double d) {
   e = fma(-d, y, 1.0);
   return fma(y, e, y);
 }
-// tanh(x) = 1 - 2 / (E + 1), E = exp(2x) <= 1e300 (E = 0 gives -1)
-__device__ __forceinline__ double tanh_from_exp2x(double E) { return fma(-2.0, rcp_newton(E + 1.0), 1.0); }
-// general argument: exp(2x) clamped below overflow (tanh is 1.0 in fp64 far before)
-__device__ __forceinline__ double tanh_fast(double x) { return tanh_from_exp2x(fmin(exp(2.0 * x), 1e300)); }
+// tanh(x) = em / (em + 2) with em = expm1(2x) in [-1, 1e300]: relative
+// accuracy for small |x| too (1 - 2 / (exp(2x) + 1) loses it to cancellation)
+__device__ __forceinline__ double tanh_from_expm1(double em) { return em * rcp_newton(em + 2.0); }
+// general argument: expm1(2x) clamped below overflow (tanh is 1.0 in fp64 far before)
+__device__ __forceinline__ double tanh_fast(double x) { return tanh_from_expm1(fmin(expm1(2.0 * x), 1e300)); }
 
 // activation value and its first two derivatives at pre (basis.py:119-126)
 __device__ __forceinline__ void activation(int act, double pre, double& tv, double& g1, double& g2) {
@@ -210,10 +209,12 @@ __device__ __forceinline__ void row_coef(const fl_assembly_desc& d, int j, int r
 // regrouped by activation derivative).
 //
 // Phase 2 (per 64-column chunk): tanh features on an interior lattice box
-// use exp(2 (x~ . W_k + b_k)) = prod_a exp(2 (x~_a W_ka [+ b_k])): the
-// per-axis factors of the lattice coordinates the tile touches are
-// tabulated once per chunk (~60 exps for 16384 entries), so an entry costs
-// D - 1 multiplies, one reciprocal (MUFU + 2 Newton steps) and ~10 FMAs,
+// use exp(2 (x~ . W_k + b_k)) = prod_a exp(2 (x~_a W_ka [+ b_k])), kept as
+// expm1 values (expm1(a + b) = e_a + e_b + e_a e_b) so tanh = em / (em + 2)
+// stays relatively accurate near 0: the per-axis factors of the lattice
+// coordinates the tile touches are tabulated once per chunk (~60 expm1 for
+// 16384 entries), so an entry costs 2 (D - 1) FMAs, one reciprocal (MUFU +
+// 2 Newton steps) and ~10 FMAs,
 // with the column terms fp, fp^2 shared by the thread's two rows; rows off
 // the lattice (constraint points), other activations and blocks whose
 // factors could overflow evaluate exp / sincos per entry.
@@ -362,12 +363,12 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
     const int nk = min(CK, K - k0);
     if (use_tab) {
       __syncthreads();
-      // tab[c * TLMAX + q] = exp(2 (x~ W_{k0+c, a} [+ b_{k0+c}])), thread -> fixed q
+      // tab[c * TLMAX + q] = expm1(2 (x~ W_{k0+c, a} [+ b_{k0+c}])), thread -> fixed q
       if (tc < tcs)
         for (int c = tc; c < nk; c += tcs) {
           double e = txa * sW[(k0 + c) * D + ta];
           if (ta == 0) e += sB[k0 + c];
-          tab[c * TLMAX + tq] = exp(2.0 * e);
+          tab[c * TLMAX + tq] = expm1(2.0 * e);
         }
       __syncthreads();
     }
@@ -381,10 +382,17 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
         double v[RPT];
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
-          double E = tab[c * TLMAX + toff[u][0]];
-          if (D > 1) E *= tab[c * TLMAX + toff[u][1]];
-          if (D > 2) E *= tab[c * TLMAX + toff[u][2]];
-          v[u] = rc[u].valid ? entry_tanh(rc[u], f1, f2, tanh_from_exp2x(E)) : 0.0;
+          // expm1 of a sum from the factors' expm1: prod (1 + e_a) - 1
+          double em = tab[c * TLMAX + toff[u][0]];
+          if (D > 1) {
+            const double e1 = tab[c * TLMAX + toff[u][1]];
+            em = fma(em, e1, em + e1);
+          }
+          if (D > 2) {
+            const double e2 = tab[c * TLMAX + toff[u][2]];
+            em = fma(em, e2, em + e2);
+          }
+          v[u] = rc[u].valid ? entry_tanh(rc[u], f1, f2, tanh_from_expm1(em)) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < RPT; u += 2)

@@ -324,9 +324,13 @@ class AdditiveSchwarz:
 
 
 def as_preconditioner(system, cutoff: float = 1e-14) -> AdditiveSchwarz:
-    """`solvers.py:181-192` on the device: Gramians A_j^T A_j from the
-    resident blocks (cuBLAS batched GEMM), eigendecomposition (cuSOLVER),
-    eigenvalues at or below cutoff * largest dropped."""
+    """`solvers.py:178-192` on the device: per block the Gramian A_j^T A_j,
+    its eigendecomposition and the pseudo-inverse over eigenvalues above
+    cutoff * the largest. K <= 96 (every paper demo): one kernel
+    (`fl_as_setup`, csrc/as_setup.cu: Gramian from the resident block,
+    parallel cyclic Jacobi in shared memory). Wider blocks: a batched
+    library eigensolver (cuBLAS Gramian + cuSOLVER syevd) — the baseline's
+    one-off setup, not on the north-star path."""
     from .assembly import adopt_system
     t = D.torch()
     system = adopt_system(system)
@@ -335,6 +339,15 @@ def as_preconditioner(system, cutoff: float = 1e-14) -> AdditiveSchwarz:
     L = st.layout
     K = L.K
     J = L.J
+    ranges = [np.arange(j * K, (j + 1) * K) for j in range(J)]
+    if K <= _lib.FL_AS_MAX_K:
+        inv = t.empty(max(J * K * K, 1), dtype=t.float64, device=st.vals.device)
+        deg = t.zeros(max(J, 1), dtype=t.int32, device=st.vals.device)
+        _lib.check(_lib.lib().fl_as_setup(C.byref(st.struct()), float(cutoff), D.ptr(inv), D.ptr(deg),
+                                          D.stream_ptr()), "fl_as_setup")
+        degenerate = np.nonzero(D.to_host(deg)[:J])[0]
+        return AdditiveSchwarz(system.column_count, ranges, None, tuple(int(j) for j in degenerate),
+                               _device=inv)
     grams = t.empty((max(J, 1), K, K), dtype=t.float64, device=st.vals.device)
     for ldv in np.unique(L.ld):
         js = np.nonzero(L.ld == ldv)[0]
@@ -351,7 +364,6 @@ def as_preconditioner(system, cutoff: float = 1e-14) -> AdditiveSchwarz:
     inv_vals = t.where(keep, 1.0 / t.where(keep, evals, t.ones_like(evals)), t.zeros_like(evals))
     inv = t.bmm(evecs * inv_vals[:, None, :], evecs.transpose(1, 2))
     degenerate = np.nonzero(~D.to_host(keep.all(dim=1)))[0]
-    ranges = [np.arange(j * K, (j + 1) * K) for j in range(J)]
     return AdditiveSchwarz(system.column_count, ranges, None, tuple(int(j) for j in degenerate),
                            _device=inv.reshape(-1).contiguous())
 

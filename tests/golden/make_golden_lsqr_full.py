@@ -6,7 +6,7 @@ Runs the reference's own stage chain on the full BASELINE cfg3 system:
 `assemble` (assembly.py:124) -> `filter_system` (filtering.py:92) ->
 `precondition` (:165) -> `lsqr` (solvers.py:87, fixed budget, the paper's
 10 000-iteration protocol) -> `recover_solution` (filtering.py:169), then
-M.a (`GlobalSystem.apply`, assembly.py:91) and the prediction on the test
+M.a (`apply`, assembly.py:91) and the prediction on the test
 lattice (`evaluate_solution` assembly.py:273 at `make_test_set` points).
 
 Keeps y, M.a, the test-lattice prediction, the phi-bar records every 100
@@ -50,13 +50,14 @@ def main(name, iters):
     res = r_sol.lsqr(op, system.rhs, iters, monitor=mon)
     t4 = time.time()
     y = res.solution
+    np.save(os.path.join("/tmp", f"lsqr_full_{name}_y.npy"), y)  # the expensive part, kept first
     a = r_filt.recover_solution(fs, y)
-    ma = system.apply(a)
+    ma = r_asm.apply(system, a)
     r = system.rhs - q @ y
     test2 = float(np.linalg.norm(q.T @ r) / (np.sqrt((q.multiply(q)).sum()) * np.linalg.norm(r)))
     ts = r_asm.make_test_set(prob, dec)
     pred = r_asm.evaluate_solution(prob, dec, basis, a, ts.points)
-    rec = np.array(mon.records, dtype=float)
+    rec = np.array(mon.records, dtype=float).reshape(-1, 3)
     np.savez_compressed(
         os.path.join(HERE, f"lsqr_full_{name}.npz"), y=y, ma=ma, pred=pred,
         records=rec[:, :2], iterations=res.iterations_run, residual=res.residual_norm,
