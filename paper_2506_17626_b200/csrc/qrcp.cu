@@ -9,9 +9,19 @@
 // over current positions (IDAMAX, swap semantics), the panel F matrix
 // (F[:, k] = tau_k A^T v_k with the incremental correction), row updates of
 // the current row, downdate temp = max(0, (1 + t)(1 - t)), t = |a_rj|/vn1_j,
-// columns with temp * (vn1/vn2)^2 <= sqrt(eps) flagged and the panel closed
-// early, their norms recomputed after the block update. Truncation: the
-// first step with |R_ii| < sigma |R_00| stops everything (linalg.py:75-85).
+// columns with temp * (vn1/vn2)^2 <= sqrt(eps) flagged; their norms are
+// recomputed at once from the panel-updated values (dlaqps closes the panel
+// and recomputes after the block update: same exact-arithmetic value,
+// DESIGN.md §3 K2). Truncation: the first step with |R_ii| < sigma |R_00|
+// stops everything (linalg.py:75-85).
+//
+// Measured and removed variants (cfg4, one filter): dlaqps's literal early
+// panel close (96.6 vs 91.3 ms then, 4x more block updates), an L2 bulk
+// prefetch of the step's trailing columns behind the argmax (115.7 vs 89.6
+// ms: evicted again before use), the reflector scaled by its readers instead
+// of once in shared memory (72.6 vs 67.5 ms), gemv column groups from a
+// shared counter (68.1 vs 67.6 ms), two 256-thread CTAs per SM (85-90 vs
+// 67.5 ms: DRAM reads 327-351 vs 230 GB, round 2).
 //
 // The step's critical path is a handful of dependent memory round trips, so
 // the kernel is organised for memory-level parallelism: the column swap is
@@ -22,7 +32,6 @@
 // panel-start matrix), and the auxv dots issue eight loads per lane at a
 // time.
 #include <float.h>
-#include <stdlib.h>
 
 #include <type_traits>
 
@@ -47,15 +56,6 @@ constexpr int NW = NT / 32;
 #ifndef QRCP_NTL
 #define QRCP_NTL 2
 #endif
-#ifndef QRCP_EARLY_CLOSE
-#define QRCP_EARLY_CLOSE 0  // 1: dlaqps's literal early panel close on a flagged norm
-#endif
-#ifndef QRCP_PREFETCH
-// 1: bulk L2 prefetch of the step's trailing columns behind the argmax.
-// Measured on cfg4: 115.7 vs 89.6 ms, DRAM reads 627 vs 376 GB (the lines
-// are evicted again before the gemv reaches them at 296 blocks in flight)
-#define QRCP_PREFETCH 0
-#endif
 #ifndef QRCP_L1KEEP
 // F-gemv loads: column groups starting < QRCP_L1KEEP trailing columns past the
 // pivot use L1::evict_last, the rest L1::no_allocate. Measured on cfg4 (one
@@ -63,16 +63,6 @@ constexpr int NW = NT / 32;
 // / 160 / 192 / 256: 76.4 / 74.8 / 74.6 / 73.2 / 74.3 / 76.0 / 78.4; all
 // evict_last 81.6
 #define QRCP_L1KEEP 128
-#endif
-#ifndef QRCP_PRESCALE
-// 1: the reflector is scaled in shared memory once per step (one barrier)
-// and the gemv / auxv read it as is; 0: scaled on the fly by its readers.
-// Measured on cfg4: on the fly 89.7 vs 91.3 with the two-CTA shape, but with
-// the L1-hinted gemv the readers' scaling dominates: 67.5 vs 72.6 ms
-#define QRCP_PRESCALE 1
-#endif
-#ifndef QRCP_DYN
-#define QRCP_DYN 0  // 1: gemv column groups from a shared counter (measured 68.1 vs 67.6 ms)
 #endif
 #ifndef QRCP_MB
 #define QRCP_MB 1
@@ -107,18 +97,10 @@ __device__ __forceinline__ double ld_keep1(const double* p) {
   asm volatile("ld.global.L1::evict_last.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
   return v;
 }
-#ifndef QRCP_HINTS2
-#define QRCP_HINTS2 1
-#endif
-#if QRCP_HINTS2
 // panel columns (re-read by the auxv dots every step of the panel) kept in
 // L1; the block update's once-per-panel read-modify-write streams past it
 #define QRCP_LD_PANEL(p) ld_keep1(p)
 #define QRCP_LD_UPD(p) ld_stream(p)
-#else
-#define QRCP_LD_PANEL(p) (*(p))
-#define QRCP_LD_UPD(p) (*reinterpret_cast<const double2*>(p))
-#endif
 
 __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
 #pragma unroll
@@ -153,7 +135,6 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   __shared__ double rowi[PB + 1];
   __shared__ int s_stop, s_rank, s_flagged, s_p;
   __shared__ double s_alpha;
-  __shared__ int s_next;
 
   double* A = q.R0 + (int64_t)j * K * K;
   double* tau = q.tau + (int64_t)j * K;
@@ -197,16 +178,6 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             bv = x;
             bi = c;
           }
-#if QRCP_PREFETCH
-          // the step's F-gemv streams rows i0..M-1 of every trailing column:
-          // start pulling them into L2 now, behind the argmax, swap and dlarfg
-          if (i + 1 < M) {
-            const int i0 = i & ~1;
-            const unsigned bytes = (unsigned)(((M - i0) * 8 + 15) & ~15);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(A + (int64_t)c * K + i0), "r"(bytes)
-                         : "memory");
-          }
-#endif
         }
         argmax_lowest(bv, bi);
         if (lane == 0) {
@@ -242,16 +213,11 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             if (kk < k) xp -= pa[kk] * F[kk * K + p];
           v[r - i] = xp;
           if (r > i) ss += xp * xp;
-#if QRCP_PRESCALE
           if (r == i) s_alpha = xp;
-#endif
         }
       }
       ss = fl::warp_sum(ss);
       if (lane == 0) red[wid] = ss;
-#if QRCP_DYN
-      if (threadIdx.x == 0) s_next = 0;
-#endif
       __syncthreads();
       // row i of the trailing columns (final once the swap is done) and of
       // the panel columns: 8-byte cp.async into shared memory, waited for
@@ -288,11 +254,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       ss = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) ss += red[w];
-#if QRCP_PRESCALE
       const double alpha = s_alpha;
-#else
-      const double alpha = v[0];
-#endif
       const double xnorm = sqrt(ss);
       double beta, t;
       if (xnorm == 0.0) {
@@ -312,11 +274,9 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         __syncthreads();
         break;
       }
-      // v = x * scal (dlarfg's dscal), v_i = 1: prescaled in shared memory, or
-      // (QRCP_PRESCALE 0) left unscaled and formed by its readers bit for bit
+      // v = x * scal (dlarfg's dscal), v_i = 1, scaled once in shared memory
+      // (one more barrier) and read as is below
       const double scal = (xnorm == 0.0) ? 1.0 : 1.0 / (alpha - beta);
-#if QRCP_PRESCALE
-      // scaled reflector in shared memory once (one more barrier), read as is below
       for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
         const double x = v[r - i] * scal;
         v[r - i] = x;
@@ -324,19 +284,12 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
       if (threadIdx.x == 0) v[0] = 1.0;
       __syncthreads();
-#else
-      for (int r = i + 1 + threadIdx.x; r < M; r += NT) ci[r] = v[r - i] * scal;  // reflector below the diagonal
-#endif
       if (threadIdx.x == 0) {
         tau[i] = t;
         ci[i] = beta;
         q.diag[(int64_t)j * K + i] = fabs(beta);
       }
-#if QRCP_PRESCALE
       auto wv = [&](int r) { return v[r - i]; };
-#else
-      auto wv = [&](int r) { return r == i ? 1.0 : v[r - i] * scal; };
-#endif
       // ---- F(i+1:N, k) = t A(i:M, i+1:N)^T v ; auxv = -t A(i:M, offset:i)^T v ----
       {
         const int ncol = N - i - 1;
@@ -344,19 +297,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         // the even row i0 <= i (row i-1 contributes v = 0); two chunks per trip
         constexpr int CU = QRCP_CU;  // columns in flight per warp
         const int i0 = i & ~1;
-#if QRCP_DYN
-        // column groups handed out by a shared counter (reset before the
-        // step's first barrier): warps that drew L1-resident or shorter
-        // groups take more, so the barrier after the gemv waits less
-        auto next_group = [&]() {
-          int gidx = 0;
-          if (lane == 0) gidx = atomicAdd(&s_next, 1);
-          return __shfl_sync(0xffffffffu, gidx, 0) * CU;
-        };
-        for (int c0 = next_group(); c0 < ncol; c0 = next_group()) {
-#else
         for (int c0 = wid * CU; c0 < ncol; c0 += NW * CU) {
-#endif
           double d[CU];
           const double* cc[CU];
 #pragma unroll
@@ -427,12 +368,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             tt = fmax(0.0, (1.0 + tt) * (1.0 - tt));
             const double rr = vn1[c] / vn2[c];
             if (tt * rr * rr <= tol3z) {
-#if QRCP_EARLY_CLOSE
-              flag[c] = 1;
-              s_flagged = 1;
-#else
               flag[atomicAdd(&s_flagged, 1)] = c;
-#endif
             } else {
               vn1[c] *= sqrt(tt);
             }
@@ -440,7 +376,6 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         }
       }
       __syncthreads();
-#if !QRCP_EARLY_CLOSE
       // ---- flagged columns: instead of closing the panel (dlaqps), their
       //      norms are recomputed now from the panel-updated values
       //      A(i+1:M, c) - A(i+1:M, offset:i+1) F(c, 0:k+1)^T, which are what
@@ -494,7 +429,6 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         if (threadIdx.x == 0) s_flagged = 0;
         __syncthreads();
       }
-#endif
       ++k;
     }
     if (s_stop) break;
@@ -567,20 +501,6 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
     }
     __syncthreads();
-#if QRCP_EARLY_CLOSE
-    // ---- recompute flagged norms over rows rk..M-1 ----
-    for (int c = rk + wid; c < N; c += NW) {
-      if (!flag[c]) continue;
-      double s2 = 0.0;
-      for (int r = rk + lane; r < M; r += 32) s2 += A[(int64_t)c * K + r] * A[(int64_t)c * K + r];
-      s2 = fl::warp_sum(s2);
-      if (lane == 0) {
-        vn1[c] = vn2[c] = (rk < M) ? sqrt(s2) : 0.0;
-        flag[c] = 0;
-      }
-    }
-    __syncthreads();
-#endif
     offset = rk;
   }
   __syncthreads();
@@ -604,9 +524,7 @@ int qrcp_r0(double* R0, int K, const int32_t* kmax, int J, double sigma, double*
   if (smem > (QRCP_MB > 1 ? 110 : 220) * 1024) return FL_ERR_INVALID;
   FL_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   QrcpArgs a{R0, K, kmax, sigma, tau, perm, rank, diag, J};
-  int grid = J;
-  if (const char* e = getenv("FEATLSQ_QRCP_GRID")) grid = max(1, min(J, atoi(e)));
-  qrcp_kernel<<<grid, NT, smem, s>>>(a);
+  qrcp_kernel<<<J, NT, smem, s>>>(a);
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
