@@ -327,8 +327,10 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
               for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
             }
           };
+#ifndef QRCP_DIAG_NOGEMV  // diagnostic timing build only: gemv loads skipped, F = 0 (wrong results)
           if (c0 < QRCP_L1KEEP) rows_loop(std::true_type{});
           else rows_loop(std::false_type{});
+#endif
           {
             const double s = fl::warp_multi_sum<CU>(d);  // lane l: column u = l / (32 / CU)
             const int u = lane / (32 / CU);
