@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
 #pragma unroll
   for (int u = 0; u < RPT; ++u)
 #pragma unroll
-    for (int a = 0; a < MAXD; ++a) toff[u][a] = a < D ? base[a] + rc[u].tix[a] - lo[a] : 0;
+    for (int a = 0; a < MAXD; ++a)  // rows off the box (padding) read slot 0, never used
+      toff[u][a] = (a < D && rc[u].on_box) ? base[a] + rc[u].tix[a] - lo[a] : 0;
   double invh[MAXD];
 #pragma unroll
   for (int a = 0; a < MAXD; ++a) invh[a] = a < D ? 1.0 / d.half[a] : 0.0;
