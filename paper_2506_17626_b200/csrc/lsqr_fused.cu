@@ -53,6 +53,41 @@ constexpr int smem_per_cta(int mb) { return mb <= 1 ? 232448 : (233472 - mb * 10
 
 __device__ __forceinline__ bool is_done(const fl_lsqr_state* st) { return *(volatile const int32_t*)&st->done; }
 
+#ifndef FL_PDL
+#define FL_PDL 1
+#endif
+// Programmatic dependent launch: the row and fused kernels of an iteration
+// are launched with programmatic stream serialization, trigger their
+// successor's launch on entry and wait for their predecessor's completion
+// (and memory flush) before touching anything it wrote — the same ordering
+// as plain stream order, with the successor's launch latency hidden.
+// Measured (ms per iteration, PDL off / row only / fused only / both): cfg4
+// 1.404 / 1.403 / 1.403 / 1.404, cfg5 1.420 / 1.421 / 1.420 / 1.416, cfg3
+// 0.1378 / 0.1360 / 0.1353 / 0.1348, cfg2 0.0430 / 0.0410 / 0.0410 / 0.0397:
+// a launch-latency win for the small configs, neutral at cfg4.
+__device__ __forceinline__ void pdl_enter() {
+#if FL_PDL
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (FL_PDL && pdl) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Warp sums of W per-lane values with a butterfly: the first log2(W) steps
 // halve the set of live columns per lane group, so W columns cost
 // 5 shuffles in total; returns in lane (32/W) c the total of column c.
@@ -87,6 +122,7 @@ __global__ void __launch_bounds__(NT, MB)
   constexpr int NW = NT / 32;
   constexpr bool KEEP = RP * W <= 6;  // tile values stay in registers between the two products
   static_assert(SL >= 2 * W, "ring too shallow");
+  pdl_enter();
   if (is_done(st)) return;
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;  // [SL][ldmax] columns of Q_j
@@ -393,6 +429,7 @@ __global__ void __launch_bounds__(NT, MB)
 // iteration `it` in the last CTA (solvers.py:120-127).
 __global__ void __launch_bounds__(256) row_kernel(fl_blockop op, fl_lsqr_vecs vec, fl_lsqr_state* st, int64_t it,
                                                  int S) {
+  pdl_enter();
   if (is_done(st)) return;
   __shared__ double sh[8];
   const double alpha = st->alpha, bprev = st->beta_prev;
@@ -514,7 +551,8 @@ int try_fused(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* st, int64
                                  (int)dyn));
     attr = dyn;
   }
-  fused_kernel<NT, RP, W, ST, MB><<<op->nblocks * S, NT, dyn, s>>>(*op, *vecs, st, it, mode, ldmax, S);
+  FL_CUDA(launch_pdl(true, fused_kernel<NT, RP, W, ST, MB>, op->nblocks * S, NT, dyn, s, *op, *vecs, st, it, mode,
+                     ldmax, S));
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
@@ -622,8 +660,7 @@ int lsqr_fused_iterate(const fl_blockop* op, fl_lsqr_vecs* vecs, fl_lsqr_state* 
   const int rg = row_grid(op);
   for (int64_t k = 0; k < count; ++k) {
     const int64_t it = first_it + k;
-    row_kernel<<<rg, 256, 0, s>>>(*op, *vecs, st, it, S);
-    FL_CHECK_LAUNCH();
+    FL_CUDA(launch_pdl(true, row_kernel, rg, 256, 0, s, *op, *vecs, st, it, S));
     int e = fused(op, vecs, st, it, 1, S, s);
     if (e) return e;
     if (mon && (e = monitor_step(mon, vecs->x, st, it, s))) return e;
