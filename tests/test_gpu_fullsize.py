@@ -26,7 +26,8 @@ cfg5; cfg1 is full size in tests/test_gpu_parity.py).
 4. cfg3 against the REFERENCE's own end-to-end run (tests/golden/
    lsqr_full_cfg3.npz: featlsq assemble -> filter_system -> lsqr 10 000 ->
    recover_solution, tests/golden/make_golden_lsqr_full.py): runs L and D
-   within the same bound as in 3.
+   within the same bound as in 3 for y, M a and the prediction; the true
+   residual ||rhs - M a|| within one iteration's worth of LSQR progress.
 """
 
 from __future__ import annotations
@@ -228,7 +229,28 @@ def test_full_size_solution_within_own_spread(fl, full, golden_dir):
     for n in names:
         assert rl[n] <= max(1e-8, 10.0 * dp[n]), n
         assert rd[n] <= max(1e-8, 10.0 * dp[n]), n
-    assert abs(ph_d - float(g["residual"])) <= max(1e-9 * ph_d, 10.0 * sp_ph)
+    # residual of the solution in the raw system, ||rhs - M a||: the reference's
+    # recurrence estimate phi-bar drifts from its true residual over 10 000
+    # iterations of sequential CSR sums (1.6e-5 relative at cfg3), the device
+    # one does not (phi-bar = ||Q y - b|| to 11 digits), so the comparison
+    # with featlsq's run is on the true residuals
+    res = {k: float(np.linalg.norm(sysd.rhs - v)) for k, v in
+           (("ref", g["ma"]), ("D", fd[1]), ("L", fl_[1]), ("P", fp[1]))}
+    sp_res = abs(res["P"] - res["D"])
+    print(f"{name} true residual ||rhs - M a||: ref {res['ref']:.12e} D {res['D']:.12e} "
+          f"L {res['L']:.12e} D' {res['P']:.12e} (featlsq phi-bar {float(g['residual']):.12e})")
+    # featlsq's run assembles with numpy (entries agree to 1e-13 of the block
+    # maximum, not to 1 ulp) and factors with this container's OpenBLAS, so
+    # its trajectory sits a fraction of an iteration away from the device
+    # runs: the residual gate is one iteration's worth of LSQR progress at
+    # 10 000 iterations (from featlsq's own phi-bar records), the 1-ulp
+    # spread when that is larger
+    rec = g["records"]
+    per_it = float(rec[-2, 1] - rec[-1, 1]) / float(rec[-1, 0] - rec[-2, 0])
+    print(f"{name}: one iteration of progress at {ITERS} = {per_it:.3e} "
+          f"({per_it / res['ref']:.2e} relative); 1-ulp residual spread {sp_res:.3e}")
+    for k in ("D", "L"):
+        assert abs(res[k] - res["ref"]) <= max(per_it, 10.0 * sp_res), k
 
 
 def test_full_size_lsqr_properties(fl, full):
