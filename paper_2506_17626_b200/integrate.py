@@ -1,10 +1,10 @@
 """Route featlsq's hot path to the B200 kernels: `enable()` / `disable()`.
 
 featlsq binds its stage functions by name at import (`runner.py:34-43`), so
-the drop-in rebinds each name in every namespace that holds it — the
+the drop-in rebinds each name in every featlsq namespace that holds it — the
 defining module (`featlsq.assembly`, `.filtering`, `.solvers`, `.linalg`),
-the package namespace (`featlsq.<name>`) and `featlsq.runner` — and nothing
-else of featlsq changes. Code that did `from featlsq.filtering import
+the package namespace, `featlsq.runner` and any other importer (e.g.
+`analysis.py` imports `as_operator`) — and nothing else of featlsq changes. Code that did `from featlsq.filtering import
 filter_system` BEFORE `enable()` keeps the reference function; call
 `enable()` first (the pytest plugin `paper_2506_17626_b200.pytest_plugin`
 does so before collection).
@@ -74,11 +74,25 @@ def _solve_one(cfg, system, phi_test, lift, test_set):
 
 
 def _targets():
+    """(module, name, replacement) for every featlsq module that binds one of
+    the stage names to featlsq's own object — the defining module, the
+    package, runner, and any other importer (e.g. analysis.py's
+    `as_operator`)."""
+    import sys
     import paper_2506_17626_b200 as b200
-    out = []
+    _modules(["assembly", "filtering", "solvers", "linalg", "runner"])
+    originals = {}
     for name, mods in _NAMES.items():
-        for mod in _modules(mods) + [featlsq]:
-            if hasattr(mod, name):
+        home = _modules(mods[:1])[0]
+        orig = _SAVED.get((home.__name__, name), (None, getattr(home, name)))[1]
+        originals[name] = orig
+    out = []
+    for modname, mod in sorted(sys.modules.items()):
+        if mod is None or not (modname == "featlsq" or modname.startswith("featlsq.")):
+            continue
+        for name, orig in originals.items():
+            cur = getattr(mod, name, None)
+            if cur is orig or cur is getattr(b200, name):
                 out.append((mod, name, getattr(b200, name)))
     runner = _modules(["runner"])[0]
     out.append((runner, "_solve_one", _solve_one))

@@ -55,6 +55,25 @@ def test_reference_suite_unmodified(fl, name):
     assert res.returncode == 0, out[-3000:]
 
 
+def test_reference_whole_suite(fl):
+    """featlsq's complete test suite (13 files: acceptance, analysis, runner,
+    CLI/config, FD wave, ... — 312 tests) under its own pytest configuration
+    (`pkg/pyproject.toml`: addopts "-m 'not extended'") with the drop-in
+    enabled: every stage function and `run_experiment` run on the device."""
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([ROOT, REF, env.get("PYTHONPATH", "")])
+    cmd = [sys.executable, "-m", "pytest", "-p", "paper_2506_17626_b200.pytest_plugin",
+           "-p", "no:cacheprovider", "--rootdir", REF_TESTS, "-m", "not extended",
+           "-o", "markers=extended: long-running acceptance checks", REF_TESTS]
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=REF_TESTS,
+                         timeout=1800)
+    out = res.stdout + res.stderr
+    print(out[-2000:])
+    assert "featlsq stage functions -> paper_2506_17626_b200" in out, "shim not active"
+    assert res.returncode == 0, out[-3000:]
+    assert " 312 passed" in out
+
+
 def test_runner_uses_device_monitor(fl, golden_dir):
     """`run_experiment` on the oscillator demo config (demos/oscillator_baseline.py)
     through the shim: `runner._solve_one` builds the K6 monitor, so no iterate
