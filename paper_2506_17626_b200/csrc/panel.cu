@@ -3,12 +3,18 @@
 // block. The panel rows P0..m-1 are factored in inner panels of w columns
 // (w = 8, 4 or 2, the widest whose rows fit in shared memory); each inner
 // panel is factored entirely in shared memory, then applied to the rest of
-// the 32-column panel in compact-WY form, 4 columns at a time. Finally the
-// panel's T factor (32 x 32, upper triangular) is built from the Gram matrix
-// V^T V, computed with DMMA over shared-memory-staged row chunks.
+// the 32-column panel in compact-WY form as two streaming DMMA passes over
+// those columns (P = V^T X, then X -= V (Tw^T P)) with the loads of four
+// 8-row chunks in flight per warp. Finally the panel's T factor (32 x 32,
+// upper triangular) is built from the Gram matrix V^T V, streamed the same
+// way (the loaded fragment of an 8-column group is both the A and the B
+// operand of its tiles), and the dlarft recurrence runs on one warp with the
+// rows of T in registers.
 //
 // Reflector convention (dlarfg): beta = -sign(alpha) hypot(alpha, ||x||),
 // tau = (beta - alpha) / beta, v = [1; x / (alpha - beta)], R_ii = beta.
+#include <stdio.h>
+
 #include "wy.cuh"
 
 namespace {
@@ -27,8 +33,6 @@ constexpr int NW = NT / 32;
 #endif
 constexpr int SMEM_S = PANEL_SMEM_KB * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
 // (measured: 256 threads at two CTAs per SM, 84 KB panels, was slower: 2.80 vs 2.25 ms per launch)
-constexpr int GC = (NB * 64) % NT == 0 ? 64 : 48;  // Gram pass row chunk (NB * GC divisible by NT)
-constexpr int GLD = GC + 4;
 
 // Sum N (a power of two <= 32) per-thread partials across the CTA; results
 // in out[0..N). Within a warp a butterfly halves the live values per lane at
@@ -109,18 +113,23 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
     if (r > 0) accumulate(0, r);
     else stash(0);
   }
-  for (int s = 0; s < W; ++s) {
+#pragma unroll
+  for (int s = 0; s < W; ++s) {  // unrolled: the row registers below are indexed statically
     block_sums<2 * W>(acc, red, sc);
     const double* rb = rowb[s & 1];
     const double alpha = rb[s];
-    const double xnorm = sqrt(sc[0]);
+    const double ss = sc[0];
     double beta, t, scal;
-    if (xnorm == 0.0) {
+    if (ss == 0.0) {
       t = 0.0;
       beta = alpha;
       scal = 1.0;
     } else {
-      beta = -copysign(hypot(alpha, xnorm), alpha);
+      // ||(alpha, x)|| from the sum of squares directly (one sqrt on the
+      // step's critical path); hypot only where the squares leave the safe range
+      const double n2 = fma(alpha, alpha, ss);
+      const double nrm = (n2 > 1e-280 && n2 < 1e280 && ss > 1e-280) ? sqrt(n2) : hypot(alpha, sqrt(ss));
+      beta = -copysign(nrm, alpha);
       t = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
@@ -140,37 +149,193 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
     }
 #pragma unroll
     for (int k = 0; k < 2 * W; ++k) acc[k] = 0.0;
+    // the row's values are read once into registers, updated, stored, and
+    // the next column's sums are formed from the registers
+#pragma unroll 2
     for (int r = threadIdx.x; r < Mq; r += NT) {
       if (r < s) continue;
+      double x[W];  // row r: reflector entries (k < s), then columns s..W-1
+#pragma unroll
+      for (int k = 0; k < W; ++k) x[k] = S[k * Mq + r];
       double v = 1.0;
       if (r == s) {
         S[s * Mq + s] = beta;
       } else {
-        v = S[s * Mq + r] * scal;
+        v = x[s] * scal;
         S[s * Mq + r] = v;
       }
-      if (t != 0.0) {
 #pragma unroll
-        for (int k = 0; k < W; ++k)
-          if (k > s) S[k * Mq + r] -= pk[k] * v;
+      for (int k = 0; k < W; ++k) {
+        if (k > s) {
+          if (t != 0.0) x[k] = fma(-pk[k], v, x[k]);
+          S[k * Mq + r] = x[k];
+        } else if (k == s) {
+          x[k] = v;
+        }
       }
       if (s + 1 < W) {
-        if (r > s + 1) accumulate(s + 1, r);
-        else if (r == s + 1) stash(s + 1);
+        if (r > s + 1) {
+          double xx = 0.0;
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (k == s + 1) xx = x[k];
+          acc[0] += xx * xx;
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            if (k > s + 1) acc[k] += xx * x[k];
+            if (k < s + 1) acc[W + k] += xx * x[k];  // reflector k (r > s + 1 > k)
+          }
+        } else if (r == s + 1) {  // row s + 1 of every column, by its owner
+#pragma unroll
+          for (int k = 0; k < W; ++k) rowb[(s + 1) & 1][k] = x[k];
+        }
       }
     }
   }
   __syncthreads();
 }
 
+// entry (r, k) of the resident inner panel's V: unit lower trapezoidal, W
+// columns of Mq rows in S (stride Mq); zero outside
+template <int W>
+__device__ __forceinline__ double vval(const double* S, int Mq, int r, int k) {
+  return (k >= W || r >= Mq || r < k) ? 0.0 : (r == k ? 1.0 : S[k * Mq + r]);
+}
+
+// X -= V (Tw^T (V^T X)) for the nrest (<= 8 NT8) panel columns X right of the
+// resident inner panel (columns c + W.. of Xj, rows c..c+Mq-1; written to
+// Aj), as two streaming passes with mma.sync m8n8k4:
+//   pass 1  P(k, u) += V(r, k) X(r, u)   m = k, n = u, reduction over rows:
+//           both fragments of a lane are rows r0 + 2 t4, r0 + 2 t4 + 1 of
+//           its column (one 16-byte load of X, the two MMA k-steps take .x/.y)
+//   pass 2  X(r, u) -= V(r, k) Z(k, u)   m = u, n = r: a lane's accumulator
+//           pair is the same 16 bytes of X (loaded, updated, stored)
+// Each warp owns UN consecutive 8-row chunks per trip with all their loads
+// in flight; the W x nrest partial sums of the warps are added in warp order.
+template <int W, int NT8>
+__device__ void apply_rest(const double* S, int Mq, const double* Tw, const double* Xj, double* Aj, int64_t ld, int c,
+                           int nrest, double* Pw, double* Zs) {
+  constexpr int UN = NT8 >= 3 ? 4 : 8 / NT8;  // 8 to 12 16-byte loads in flight per lane
+  constexpr int PC = 8 * NT8;                  // padded column count
+  constexpr int KS = (W + 3) / 4;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  const int nch = (Mq + 7) / 8;
+  const int x0 = c + W;
+  const double* xcol[NT8];
+  bool cok[NT8];
+#pragma unroll
+  for (int t = 0; t < NT8; ++t) {
+    cok[t] = 8 * t + g < nrest;
+    xcol[t] = Xj + (int64_t)(x0 + (cok[t] ? 8 * t + g : 0)) * ld + c + 2 * t4;
+  }
+  auto load_chunks = [&](int ch0, double2 (&x)[UN][NT8]) {
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int r = (ch0 + u) * 8 + 2 * t4;
+#pragma unroll
+      for (int t = 0; t < NT8; ++t) {
+        double2 v = make_double2(0.0, 0.0);
+        if (ch0 + u < nch && cok[t]) v = *reinterpret_cast<const double2*>(xcol[t] + (ch0 + u) * 8);
+        if (r >= Mq) v.x = 0.0;
+        if (r + 1 >= Mq) v.y = 0.0;
+        x[u][t] = v;
+      }
+    }
+  };
+  // ---- pass 1 ----
+  {
+    double acc[NT8][2];
+#pragma unroll
+    for (int t = 0; t < NT8; ++t) acc[t][0] = acc[t][1] = 0.0;
+    for (int ch0 = wid * UN; ch0 < nch; ch0 += NW * UN) {
+      double2 x[UN][NT8];
+      load_chunks(ch0, x);
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        const int r = (ch0 + u) * 8 + 2 * t4;
+        const double v0 = vval<W>(S, Mq, r, g), v1 = vval<W>(S, Mq, r + 1, g);
+#pragma unroll
+        for (int t = 0; t < NT8; ++t) {
+          fl::dmma(acc[t][0], acc[t][1], v0, x[u][t].x);
+          fl::dmma(acc[t][0], acc[t][1], v1, x[u][t].y);
+        }
+      }
+    }
+    if (g < W) {
+#pragma unroll
+      for (int t = 0; t < NT8; ++t) {
+        Pw[(wid * W + g) * PC + 8 * t + 2 * t4] = acc[t][0];
+        Pw[(wid * W + g) * PC + 8 * t + 2 * t4 + 1] = acc[t][1];
+      }
+    }
+  }
+  __syncthreads();
+  // P = sum over warps (fixed order); Z = Tw^T P (Tw^T[k][b] = Tw[k * W + b], b <= k)
+  for (int o = threadIdx.x; o < W * PC; o += NT) {
+    double p = 0.0;
+    for (int w = 0; w < NW; ++w) p += Pw[w * W * PC + o];
+    Zs[o] = p;
+  }
+  __syncthreads();
+  double az[NT8][KS];  // -Z(k = t4 + 4 s, u = 8 t + g)
+#pragma unroll
+  for (int t = 0; t < NT8; ++t)
+#pragma unroll
+    for (int s2 = 0; s2 < KS; ++s2) {
+      const int k = t4 + 4 * s2;
+      double z = 0.0;
+      if (k < W)
+        for (int b = 0; b <= k; ++b) z += Tw[k * W + b] * Zs[b * PC + 8 * t + g];
+      az[t][s2] = -z;
+    }
+  // ---- pass 2 ----
+  for (int ch0 = wid * UN; ch0 < nch; ch0 += NW * UN) {
+    double2 x[UN][NT8];
+    load_chunks(ch0, x);
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int rb = (ch0 + u) * 8 + g;
+      double vb[KS];
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) vb[s2] = vval<W>(S, Mq, rb, t4 + 4 * s2);
+#pragma unroll
+      for (int t = 0; t < NT8; ++t) {
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) fl::dmma(x[u][t].x, x[u][t].y, az[t][s2], vb[s2]);
+        const int r = (ch0 + u) * 8 + 2 * t4;
+        if (ch0 + u < nch && cok[t] && r < Mq)
+          *reinterpret_cast<double2*>(Aj + (int64_t)(x0 + 8 * t + g) * ld + c + r) = x[u][t];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+#ifdef PANEL_PHASES  // diagnostic build: cycles per phase (thread 0's clock)
+#define PPH(n)                                 \
+  do {                                         \
+    if (threadIdx.x == 0) {                    \
+      const long long t_ = clock64();          \
+      ph_acc[n] += t_ - ph_last;               \
+      ph_last = t_;                            \
+    }                                          \
+  } while (0)
+#else
+#define PPH(n)
+#endif
+
 template <int W>
 __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, double* sc, double* Tw,
-                           double* Vs, double* Gs) {
+                           double* Gs, double* Pw, double* Zs) {
   const int m = a.m[j];
   const int64_t ld = a.ld[j];
   double* Aj = a.A + a.off[j];
   double* tau_j = a.tau + (int64_t)j * a.K;
   const int P0 = a.P0;
+#ifdef PANEL_PHASES
+  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+#endif
   for (int q = 0; q < NB / W; ++q) {
     const int c = P0 + q * W;
     const int Mq = m - c;
@@ -186,181 +351,137 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
       }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
+    PPH(0);
     factor_inner<W>(S, Mq, red, sc, Tw, tau_j, c);
+    PPH(1);
     for (int k = 0; k < W; ++k)
       for (int r = threadIdx.x; r < Mq; r += NT) Aj[(int64_t)(c + k) * ld + c + r] = S[k * Mq + r];
-    // apply (I - V Tw V^T)^T to the panel columns right of this inner panel,
-    // 4 at a time: one pass per group updates group g (with z(g) = Tw^T
-    // V^T x(g)) and forms the dots V^T x(g+1) of the next group from the same
-    // rows (thread r mod NT throughout), so the groups cost one pass and one
-    // reduction each instead of two passes
+    PPH(2);
+    // apply (I - V Tw V^T)^T to the panel columns right of this inner panel
     {
-      const int ng = (P0 + NB - (c + W)) / 4;
-      __shared__ double z[2][4 * 8];
-      auto vvals = [&](int r, double (&vv)[W]) {
-#pragma unroll
-        for (int k = 0; k < W; ++k) vv[k] = (r < k) ? 0.0 : ((r == k) ? 1.0 : S[k * Mq + r]);
-      };
-      auto finish = [&](double (&p)[4 * W], int buf) {  // z(buf) = Tw^T (V^T x)
-        block_sums<4 * W>(p, red, sc);
-        if (threadIdx.x < 4 * W) {
-          const int k = threadIdx.x / 4, u = threadIdx.x % 4;
-          double s2 = 0.0;
-          for (int b = 0; b <= k; ++b) s2 += Tw[k * W + b] * sc[b * 4 + u];  // Tw^T[k][b] = Tw[b][k]
-          z[buf][k * 4 + u] = s2;
-        }
-        __syncthreads();
-      };
-      if (ng > 0) {
-        double p[4 * W];
-#pragma unroll
-        for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
-        const int x0 = c + W;
-#pragma unroll 2
-        for (int r = threadIdx.x; r < Mq; r += NT) {
-          double vv[W], xv[4];
-          vvals(r, vv);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) xv[u] = Xj[(int64_t)(x0 + u) * ld + c + r];
-#pragma unroll
-          for (int k = 0; k < W; ++k)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p[k * 4 + u] += vv[k] * xv[u];
-        }
-        finish(p, 0);
-      }
-      for (int gi = 0; gi < ng; ++gi) {
-        const int x0 = c + W + 4 * gi;
-        const bool nxt = gi + 1 < ng;
-        const volatile double* zg = z[gi & 1];  // re-read per row (hoisted it would pin 4W registers)
-        double p[4 * W];
-#pragma unroll
-        for (int k = 0; k < 4 * W; ++k) p[k] = 0.0;
-#pragma unroll 1
-        for (int r = threadIdx.x; r < Mq; r += NT) {
-          double vv[W], xn[4];
-          vvals(r, vv);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) xn[u] = nxt ? Xj[(int64_t)(x0 + 4 + u) * ld + c + r] : 0.0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            double s2 = 0.0;
-#pragma unroll
-            for (int k = 0; k < W; ++k) s2 += vv[k] * zg[k * 4 + u];
-            Aj[(int64_t)(x0 + u) * ld + c + r] = Xj[(int64_t)(x0 + u) * ld + c + r] - s2;
-          }
-          if (nxt) {
-#pragma unroll
-            for (int k = 0; k < W; ++k)
-#pragma unroll
-              for (int u = 0; u < 4; ++u) p[k * 4 + u] += vv[k] * xn[u];
-          }
-        }
-        if (nxt) finish(p, (gi + 1) & 1);
-        else __syncthreads();
-      }
+      const int nrest = P0 + NB - (c + W);
+      const int nt8 = (nrest + 7) / 8;
+      if (nt8 == 4) apply_rest<W, 4>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      else if (nt8 == 3) apply_rest<W, 3>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      else if (nt8 == 2) apply_rest<W, 2>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      else if (nt8 == 1) apply_rest<W, 1>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      PPH(4);
     }
   }
-  // ---- T for the 32-column panel from G = V^T V (DMMA over staged chunks) ----
-  __syncthreads();  // every inner panel written back; S is reused as the staging buffer
+  // ---- T for the 32-column panel from G = V^T V, streamed with DMMA ----
+  __syncthreads();  // every inner panel written back; S is reused for the warps' partial tiles
   const int M = m - P0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
-  // upper-triangular 8x8 tiles (ta <= tb): 10 tiles, tile w and (with fewer
-  // than 10 warps) tile w + NW per warp
-  constexpr int NTW = (10 + NW - 1) / NW;
-  int ta[NTW], tb[NTW];
+  {
+    // a lane loads rows r0 + 2 t4, r0 + 2 t4 + 1 of columns 8 c4 + g (c4 = 0..3):
+    // that fragment is the A operand of the tiles (c4, *) and the B operand
+    // of the tiles (*, c4); the 10 upper tiles (ta <= tb) are accumulated
+    constexpr int UG = 2;
+    const int nch = (M + 7) / 8;
+    double acc[10][2];
 #pragma unroll
-  for (int q = 0; q < NTW; ++q) {
-    ta[q] = tb[q] = -1;
-    int idx = w + q * NW, cnt = 0;
-    for (int x = 0; x < 4; ++x)
-      for (int y = x; y < 4; ++y) {
-        if (cnt == idx) {
-          ta[q] = x;
-          tb[q] = y;
+    for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const double* vcol = Aj + (int64_t)(P0 + g) * ld + P0 + 2 * t4;
+    for (int ch0 = w * UG; ch0 < nch; ch0 += NW * UG) {
+      double2 x[UG][4];
+#pragma unroll
+      for (int u = 0; u < UG; ++u)
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4)
+          x[u][c4] = (ch0 + u < nch) ? *reinterpret_cast<const double2*>(vcol + (int64_t)(8 * c4) * ld + (ch0 + u) * 8)
+                                     : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        const int r = (ch0 + u) * 8 + 2 * t4;
+        if ((ch0 + u) * 8 < NB || (ch0 + u) * 8 + 8 > M) {  // unit diagonal, zeros above it and past row M
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const int col = 8 * c4 + g;
+            if (r >= M || r < col) x[u][c4].x = 0.0;
+            else if (r == col) x[u][c4].x = 1.0;
+            if (r + 1 >= M || r + 1 < col) x[u][c4].y = 0.0;
+            else if (r + 1 == col) x[u][c4].y = 1.0;
+          }
         }
-        ++cnt;
-      }
-  }
-  double acc[NTW][2];
+        int t = 0;
 #pragma unroll
-  for (int q = 0; q < NTW; ++q) acc[q][0] = acc[q][1] = 0.0;
-  // the next chunk's V values are loaded into registers while this one is
-  // multiplied (one round trip per chunk overlapped instead of exposed)
-  constexpr int PER = NB * GC / NT;
-  static_assert(PER * NT == NB * GC, "chunk must split evenly over the CTA");
-  double nx[PER];
-  auto fetch = [&](int r0) {
+        for (int ta = 0; ta < 4; ++ta)
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int p = threadIdx.x + q * NT, col = p / GC, rr = p % GC, row = r0 + rr;
-      double v = 0.0;
-      if (row < M) {
-        if (row > col) v = Aj[(int64_t)(P0 + col) * ld + P0 + row];
-        else if (row == col) v = 1.0;
+          for (int tb = ta; tb < 4; ++tb) {
+            fl::dmma(acc[t][0], acc[t][1], x[u][ta].x, x[u][tb].x);
+            fl::dmma(acc[t][0], acc[t][1], x[u][ta].y, x[u][tb].y);
+            ++t;
+          }
       }
-      nx[q] = v;
     }
-  };
-  fetch(0);
-  for (int r0 = 0; r0 < M; r0 += GC) {
+    double* Pg = S;  // (NW, 10, 64)
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int p = threadIdx.x + q * NT;
-      Vs[(p / GC) * GLD + p % GC] = nx[q];
-    }
-    if (r0 + GC < M) fetch(r0 + GC);
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < NTW; ++q) {
-      if (ta[q] >= 0) {
-#pragma unroll 4
-        for (int k0 = 0; k0 < GC; k0 += 4)
-          fl::dmma(acc[q][0], acc[q][1], Vs[(ta[q] * 8 + g) * GLD + k0 + t4], Vs[(tb[q] * 8 + g) * GLD + k0 + t4]);
-      }
+    for (int t = 0; t < 10; ++t) {
+      Pg[(w * 10 + t) * 64 + g * 8 + 2 * t4] = acc[t][0];
+      Pg[(w * 10 + t) * 64 + g * 8 + 2 * t4 + 1] = acc[t][1];
     }
     __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < NTW; ++q) {
-    if (ta[q] >= 0) {
-      Gs[(ta[q] * 8 + g) * NB + tb[q] * 8 + 2 * t4] = acc[q][0];
-      Gs[(ta[q] * 8 + g) * NB + tb[q] * 8 + 2 * t4 + 1] = acc[q][1];
+    for (int o = threadIdx.x; o < 640; o += NT) {
+      const int t = o / 64, i = (o % 64) / 8, jj = o % 8;
+      int ta = 0, tb = 0, cnt = 0;
+      for (int x2 = 0; x2 < 4; ++x2)
+        for (int y2 = x2; y2 < 4; ++y2) {
+          if (cnt == t) {
+            ta = x2;
+            tb = y2;
+          }
+          ++cnt;
+        }
+      double sum = 0.0;
+      for (int ww = 0; ww < NW; ++ww) sum += Pg[(ww * 10 + t) * 64 + i * 8 + jj];
+      Gs[(ta * 8 + i) * NB + tb * 8 + jj] = sum;
     }
   }
   __syncthreads();
+  PPH(5);
   if (w == 0) {
-    // T (column-major) : T[i][i] = tau_i; T[0:i,i] = -tau_i T[0:i,0:i] G[0:i,i]
+    // dlarft (forward, columnwise): T[i][i] = tau_i; T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i].
+    // Lane a keeps row a of T in registers (zero left of the diagonal).
     double* Tp = a.T + ((int64_t)j * (a.K / NB) + P0 / NB) * NB * NB;
-    double* Tl = S;  // the staging buffer is free once G is formed
+    const double tl = tau_j[P0 + lane];
+    double Tr[NB];
+#pragma unroll
     for (int i = 0; i < NB; ++i) {
-      const double ti = tau_j[P0 + i];
-      double z = 0.0;
-      if (lane < i)
-        for (int b = lane; b < i; ++b) z += Tl[b * NB + lane] * Gs[b * NB + i];
-      __syncwarp();
-      Tl[i * NB + lane] = (lane < i) ? -ti * z : (lane == i ? ti : 0.0);
-      __syncwarp();
+      const double ti = __shfl_sync(0xffffffffu, tl, i);
+      double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < i; ++b) {
+        if (b & 1) z1 = fma(Tr[b], Gs[b * NB + i], z1);
+        else z0 = fma(Tr[b], Gs[b * NB + i], z0);
+      }
+      Tr[i] = (lane < i) ? -ti * (z0 + z1) : (lane == i ? ti : 0.0);
+      Tp[i * NB + lane] = Tr[i];
     }
-    for (int i = lane; i < NB * NB; i += 32) Tp[i] = Tl[i];
   }
+#ifdef PANEL_PHASES
+  PPH(6);
+  if (threadIdx.x == 0 && (j % 256) == 5)
+    printf("PANELPH j=%d P0=%d W=%d M=%d load=%lld factor=%lld wb=%lld dots0=%lld groups=%lld gram=%lld tbuild=%lld\n", j, P0,
+           W, m - P0, ph_acc[0], ph_acc[1], ph_acc[2], ph_acc[3], ph_acc[4], ph_acc[5], ph_acc[6]);
+#endif
 }
 
 __global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
   extern __shared__ double sm[];
   double* S = sm;                                   // SMEM_S bytes
-  double* Vs = sm;                                  // reuses S for the Gram pass
   __shared__ double red[NW * 32];
   __shared__ double sc[64];
   __shared__ double Tw[64];
-  __shared__ double Gs[NB * NB];
+  __shared__ double Pw[NW * 8 * 24];  // apply_rest's per-warp partial sums; G of the finished panel
+  __shared__ double Zs[256];
+  double* Gs = Pw;
   const int j = blockIdx.x;
   const int M = a.m[j] - a.P0;
   if (M <= 0) return;
   const int cap = SMEM_S / 8;
-  if (8 * M <= cap) panel_body<8>(a, j, S, red, sc, Tw, Vs, Gs);
-  else if (4 * M <= cap) panel_body<4>(a, j, S, red, sc, Tw, Vs, Gs);
-  else if (2 * M <= cap) panel_body<2>(a, j, S, red, sc, Tw, Vs, Gs);
+  if (8 * M <= cap) panel_body<8>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
+  else if (4 * M <= cap) panel_body<4>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
+  else if (2 * M <= cap) panel_body<2>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
   else __trap();  // excluded by rrqr_route (filtering.py BLOCKED_MAX_ROWS) and panel_factor
 }
 

@@ -32,6 +32,7 @@
 // panel-start matrix), and the auxv dots issue eight loads per lane at a
 // time.
 #include <float.h>
+#include <stdio.h>
 
 #include <type_traits>
 
@@ -114,8 +115,26 @@ __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
   }
 }
 
+#ifdef QRCP_PHASES  // diagnostic build: cycles per phase of the pivot step (thread 0's clock)
+#define PH(n)                                  \
+  do {                                         \
+    if (threadIdx.x == 0) {                    \
+      const long long t_ = clock64();          \
+      ph_acc[n] += t_ - ph_last;               \
+      ph_last = t_;                            \
+    }                                          \
+  } while (0)
+#else
+#define PH(n)
+#endif
+
 __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   extern __shared__ double sm[];
+#ifdef QRCP_PHASES
+  long long ph_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+  int ph_steps = 0, ph_flag = 0;
+#endif
   const int K = q.K;
   for (int j = blockIdx.x; j < q.J; j += gridDim.x) {
   const int M = q.kmax[j];
@@ -191,6 +210,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         argmax_lowest(bv, bi);
         s_pl = bi;
       }
+      PH(0);
       const int p = s_pl;
       // ---- swap columns i <-> p fused with the pivot column's panel update:
       //      v = A(i:M, p) - A(i:M, offset:i) F(p, 0:k)^T ----
@@ -219,6 +239,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       ss = fl::warp_sum(ss);
       if (lane == 0) red[wid] = ss;
       __syncthreads();
+      PH(1);
       // row i of the trailing columns (final once the swap is done) and of
       // the panel columns: 8-byte cp.async into shared memory, waited for
       // only before the row update, so the round trip overlaps dlarfg and the
@@ -284,6 +305,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
       if (threadIdx.x == 0) v[0] = 1.0;
       __syncthreads();
+      PH(2);
       if (threadIdx.x == 0) {
         tau[i] = t;
         ci[i] = beta;
@@ -337,6 +359,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
             if ((lane & (32 / CU - 1)) == 0 && c0 + u < ncol) F[k * K + i + 1 + c0 + u] = t * s;
           }
         }
+        PH(3);
         for (int kk = wid; kk < k; kk += NW) {
           const double* cc = A + (int64_t)(offset + kk) * K;
           double dd = 0.0;
@@ -352,9 +375,11 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           if (lane == 0) auxv[kk] = -t * dd;
         }
         if (threadIdx.x == k) rowi[k] = 1.0;
+        PH(4);
         asm volatile("cp.async.wait_all;\n" ::: "memory");
       }
       __syncthreads();
+      PH(5);
       // ---- F(:, k) += F(:, 0:k) auxv (F(offset..i, k) = 0 first);
       //      A(i, i+1:N) -= A(i, offset:i+1) F(i+1:N, 0:k+1)^T ; downdate ----
       for (int c = offset + threadIdx.x; c < N; c += NT) {
@@ -378,6 +403,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         }
       }
       __syncthreads();
+      PH(6);
       // ---- flagged columns: instead of closing the panel (dlaqps), their
       //      norms are recomputed now from the panel-updated values
       //      A(i+1:M, c) - A(i+1:M, offset:i+1) F(c, 0:k+1)^T, which are what
@@ -430,7 +456,14 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
         }
         if (threadIdx.x == 0) s_flagged = 0;
         __syncthreads();
+#ifdef QRCP_PHASES
+        ++ph_flag;
+#endif
       }
+      PH(7);
+#ifdef QRCP_PHASES
+      ++ph_steps;
+#endif
       ++k;
     }
     if (s_stop) break;
@@ -503,6 +536,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
     }
     __syncthreads();
+    PH(8);
     offset = rk;
   }
   __syncthreads();
@@ -514,6 +548,13 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
   }
   if (threadIdx.x == 0) q.rank[j] = rank;
   __syncthreads();
+#ifdef QRCP_PHASES
+  PH(9);
+  if (threadIdx.x == 0 && (j % 128) == 5)
+    printf("QRCPPH j=%d steps=%d flagged=%d argmax=%lld pivcol=%lld dlarfg=%lld gemv=%lld auxv=%lld wait=%lld rowupd=%lld flag=%lld blockupd=%lld other=%lld\n",
+           j, ph_steps, ph_flag, ph_acc[0], ph_acc[1], ph_acc[2], ph_acc[3], ph_acc[4], ph_acc[5], ph_acc[6],
+           ph_acc[7], ph_acc[8], ph_acc[9]);
+#endif
   }
 }
 
