@@ -204,60 +204,83 @@ __device__ __forceinline__ double vval(const double* S, int Mq, int r, int k) {
 
 // X -= V (Tw^T (V^T X)) for the nrest (<= 8 NT8) panel columns X right of the
 // resident inner panel (columns c + W.. of Xj, rows c..c+Mq-1; written to
-// Aj), as two streaming passes with mma.sync m8n8k4:
+// Aj), as two streaming passes with mma.sync m8n8k4 over 16-row chunks. A
+// lane's 256-bit access is rows r0 + 4 t4 .. + 3 of its column (a warp
+// access covers one full line per column):
 //   pass 1  P(k, u) += V(r, k) X(r, u)   m = k, n = u, reduction over rows:
-//           both fragments of a lane are rows r0 + 2 t4, r0 + 2 t4 + 1 of
-//           its column (one 16-byte load of X, the two MMA k-steps take .x/.y)
-//   pass 2  X(r, u) -= V(r, k) Z(k, u)   m = u, n = r: a lane's accumulator
-//           pair is the same 16 bytes of X (loaded, updated, stored)
-// Each warp owns UN consecutive 8-row chunks per trip with all their loads
-// in flight; the W x nrest partial sums of the warps are added in warp order.
+//           the four MMA k-steps take the four loaded rows in turn
+//   pass 2  X(r, u) -= V(r, k) Z(k, u)   m = u, n = r: two MMA tiles whose
+//           accumulator pairs are the loaded rows (0, 1) and (2, 3), i.e.
+//           tile h holds rows r0 + 4 (n / 2) + 2 h + n % 2
+// Each warp owns UN consecutive chunks per trip with all their loads in
+// flight; the W x nrest partial sums of the warps are added in warp order.
+#ifdef PANEL_PHASES
+__shared__ long long g_dbg[4];
+#define APH(n, t0) do { if (threadIdx.x == 0) { const long long t_ = clock64(); g_dbg[n] += t_ - t0; t0 = t_; } } while (0)
+#else
+#define APH(n, t0)
+#endif
+
+#ifndef PANEL_LD
+#define PANEL_LD 6
+#endif
+
 template <int W, int NT8>
 __device__ void apply_rest(const double* S, int Mq, const double* Tw, const double* Xj, double* Aj, int64_t ld, int c,
                            int nrest, double* Pw, double* Zs) {
-  constexpr int UN = NT8 >= 3 ? 4 : 8 / NT8;  // 8 to 12 16-byte loads in flight per lane
-  constexpr int PC = 8 * NT8;                  // padded column count
+  constexpr int UN = PANEL_LD / NT8 > 0 ? PANEL_LD / NT8 : 1;  // ~PANEL_LD 256-bit loads in flight per lane
+  constexpr int PC = 8 * NT8;                                  // padded column count
   constexpr int KS = (W + 3) / 4;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
-  const int nch = (Mq + 7) / 8;
+  // chunks start at the 4-row boundary at or above row c (W = 2: c may be
+  // 2 mod 4); rows above c (r < 0) meet V = 0 and are stored back unchanged
+  const int rsh = W >= 4 ? 0 : (c & 3);
+  const int nch = (Mq + rsh + 15) / 16;
   const int x0 = c + W;
   const double* xcol[NT8];
   bool cok[NT8];
 #pragma unroll
   for (int t = 0; t < NT8; ++t) {
     cok[t] = 8 * t + g < nrest;
-    xcol[t] = Xj + (int64_t)(x0 + (cok[t] ? 8 * t + g : 0)) * ld + c + 2 * t4;
+    xcol[t] = Xj + (int64_t)(x0 + (cok[t] ? 8 * t + g : 0)) * ld + (c - rsh) + 4 * t4;
   }
-  auto load_chunks = [&](int ch0, double2 (&x)[UN][NT8]) {
+  auto load_chunks = [&](int ch0, fl::d4 (&x)[UN][NT8]) {
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
-      const int r = (ch0 + u) * 8 + 2 * t4;
+      const int r = (ch0 + u) * 16 + 4 * t4 - rsh;
 #pragma unroll
       for (int t = 0; t < NT8; ++t) {
-        double2 v = make_double2(0.0, 0.0);
-        if (ch0 + u < nch && cok[t]) v = *reinterpret_cast<const double2*>(xcol[t] + (ch0 + u) * 8);
-        if (r >= Mq) v.x = 0.0;
-        if (r + 1 >= Mq) v.y = 0.0;
+        fl::d4 v{0.0, 0.0, 0.0, 0.0};
+        if (r < Mq && cok[t]) v = fl::ldg256(xcol[t] + (ch0 + u) * 16);
+        if (r + 1 >= Mq) v.b = 0.0;
+        if (r + 2 >= Mq) v.c = 0.0;
+        if (r + 3 >= Mq) v.d = 0.0;
         x[u][t] = v;
       }
     }
   };
+#ifdef PANEL_PHASES
+  long long tph = clock64();
+#endif
   // ---- pass 1 ----
   {
     double acc[NT8][2];
 #pragma unroll
     for (int t = 0; t < NT8; ++t) acc[t][0] = acc[t][1] = 0.0;
     for (int ch0 = wid * UN; ch0 < nch; ch0 += NW * UN) {
-      double2 x[UN][NT8];
+      fl::d4 x[UN][NT8];
       load_chunks(ch0, x);
 #pragma unroll
       for (int u = 0; u < UN; ++u) {
-        const int r = (ch0 + u) * 8 + 2 * t4;
+        const int r = (ch0 + u) * 16 + 4 * t4 - rsh;
         const double v0 = vval<W>(S, Mq, r, g), v1 = vval<W>(S, Mq, r + 1, g);
+        const double v2 = vval<W>(S, Mq, r + 2, g), v3 = vval<W>(S, Mq, r + 3, g);
 #pragma unroll
         for (int t = 0; t < NT8; ++t) {
-          fl::dmma(acc[t][0], acc[t][1], v0, x[u][t].x);
-          fl::dmma(acc[t][0], acc[t][1], v1, x[u][t].y);
+          fl::dmma(acc[t][0], acc[t][1], v0, x[u][t].a);
+          fl::dmma(acc[t][0], acc[t][1], v1, x[u][t].b);
+          fl::dmma(acc[t][0], acc[t][1], v2, x[u][t].c);
+          fl::dmma(acc[t][0], acc[t][1], v3, x[u][t].d);
         }
       }
     }
@@ -270,6 +293,7 @@ __device__ void apply_rest(const double* S, int Mq, const double* Tw, const doub
     }
   }
   __syncthreads();
+  APH(0, tph);
   // P = sum over warps (fixed order); Z = Tw^T P (Tw^T[k][b] = Tw[k * W + b], b <= k)
   for (int o = threadIdx.x; o < W * PC; o += NT) {
     double p = 0.0;
@@ -288,27 +312,34 @@ __device__ void apply_rest(const double* S, int Mq, const double* Tw, const doub
         for (int b = 0; b <= k; ++b) z += Tw[k * W + b] * Zs[b * PC + 8 * t + g];
       az[t][s2] = -z;
     }
+  APH(1, tph);
   // ---- pass 2 ----
   for (int ch0 = wid * UN; ch0 < nch; ch0 += NW * UN) {
-    double2 x[UN][NT8];
+    fl::d4 x[UN][NT8];
     load_chunks(ch0, x);
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
-      const int rb = (ch0 + u) * 8 + g;
-      double vb[KS];
+      const int rb = (ch0 + u) * 16 + 4 * (g >> 1) + (g & 1) - rsh;
+      double vb[2][KS];
 #pragma unroll
-      for (int s2 = 0; s2 < KS; ++s2) vb[s2] = vval<W>(S, Mq, rb, t4 + 4 * s2);
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) vb[h][s2] = vval<W>(S, Mq, rb + 2 * h, t4 + 4 * s2);
+      const int r = (ch0 + u) * 16 + 4 * t4 - rsh;
 #pragma unroll
       for (int t = 0; t < NT8; ++t) {
 #pragma unroll
-        for (int s2 = 0; s2 < KS; ++s2) fl::dmma(x[u][t].x, x[u][t].y, az[t][s2], vb[s2]);
-        const int r = (ch0 + u) * 8 + 2 * t4;
-        if (ch0 + u < nch && cok[t] && r < Mq)
-          *reinterpret_cast<double2*>(Aj + (int64_t)(x0 + 8 * t + g) * ld + c + r) = x[u][t];
+        for (int s2 = 0; s2 < KS; ++s2) {
+          fl::dmma(x[u][t].a, x[u][t].b, az[t][s2], vb[0][s2]);
+          fl::dmma(x[u][t].c, x[u][t].d, az[t][s2], vb[1][s2]);
+        }
+        if (cok[t] && r < Mq) fl::stg256(Aj + (int64_t)(x0 + 8 * t + g) * ld + c + r, x[u][t]);
       }
     }
   }
+  APH(2, tph);
   __syncthreads();
+  APH(3, tph);
 }
 
 #ifdef PANEL_PHASES  // diagnostic build: cycles per phase (thread 0's clock)
@@ -335,6 +366,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
 #ifdef PANEL_PHASES
   long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ph_last = clock64();
+  if (threadIdx.x == 0) g_dbg[0] = g_dbg[1] = g_dbg[2] = g_dbg[3] = 0;
 #endif
   for (int q = 0; q < NB / W; ++q) {
     const int c = P0 + q * W;
@@ -373,46 +405,45 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
   const int M = m - P0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
   {
-    // a lane loads rows r0 + 2 t4, r0 + 2 t4 + 1 of columns 8 c4 + g (c4 = 0..3):
+    // a lane loads rows r0 + 4 t4 .. + 3 of columns 8 c4 + g (c4 = 0..3):
     // that fragment is the A operand of the tiles (c4, *) and the B operand
     // of the tiles (*, c4); the 10 upper tiles (ta <= tb) are accumulated
-    constexpr int UG = 2;
-    const int nch = (M + 7) / 8;
+    const int nch = (M + 15) / 16;
     double acc[10][2];
 #pragma unroll
     for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
-    const double* vcol = Aj + (int64_t)(P0 + g) * ld + P0 + 2 * t4;
-    for (int ch0 = w * UG; ch0 < nch; ch0 += NW * UG) {
-      double2 x[UG][4];
+    const double* vcol = Aj + (int64_t)(P0 + g) * ld + P0 + 4 * t4;
+    for (int ch = w; ch < nch; ch += NW) {
+      const int r = ch * 16 + 4 * t4;
+      fl::d4 x[4];
 #pragma unroll
-      for (int u = 0; u < UG; ++u)
+      for (int c4 = 0; c4 < 4; ++c4)
+        x[c4] = (r < M) ? fl::ldg256(vcol + (int64_t)(8 * c4) * ld + ch * 16) : fl::d4{0.0, 0.0, 0.0, 0.0};
+      if (ch * 16 < NB || ch * 16 + 16 > M) {  // unit diagonal, zeros above it and past row M
+        auto fix = [&](double& v, int row, int col) {
+          if (row >= M || row < col) v = 0.0;
+          else if (row == col) v = 1.0;
+        };
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4)
-          x[u][c4] = (ch0 + u < nch) ? *reinterpret_cast<const double2*>(vcol + (int64_t)(8 * c4) * ld + (ch0 + u) * 8)
-                                     : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int u = 0; u < UG; ++u) {
-        const int r = (ch0 + u) * 8 + 2 * t4;
-        if ((ch0 + u) * 8 < NB || (ch0 + u) * 8 + 8 > M) {  // unit diagonal, zeros above it and past row M
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            const int col = 8 * c4 + g;
-            if (r >= M || r < col) x[u][c4].x = 0.0;
-            else if (r == col) x[u][c4].x = 1.0;
-            if (r + 1 >= M || r + 1 < col) x[u][c4].y = 0.0;
-            else if (r + 1 == col) x[u][c4].y = 1.0;
-          }
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int col = 8 * c4 + g;
+          fix(x[c4].a, r, col);
+          fix(x[c4].b, r + 1, col);
+          fix(x[c4].c, r + 2, col);
+          fix(x[c4].d, r + 3, col);
         }
-        int t = 0;
-#pragma unroll
-        for (int ta = 0; ta < 4; ++ta)
-#pragma unroll
-          for (int tb = ta; tb < 4; ++tb) {
-            fl::dmma(acc[t][0], acc[t][1], x[u][ta].x, x[u][tb].x);
-            fl::dmma(acc[t][0], acc[t][1], x[u][ta].y, x[u][tb].y);
-            ++t;
-          }
       }
+      int t = 0;
+#pragma unroll
+      for (int ta = 0; ta < 4; ++ta)
+#pragma unroll
+        for (int tb = ta; tb < 4; ++tb) {
+          fl::dmma(acc[t][0], acc[t][1], x[ta].a, x[tb].a);
+          fl::dmma(acc[t][0], acc[t][1], x[ta].b, x[tb].b);
+          fl::dmma(acc[t][0], acc[t][1], x[ta].c, x[tb].c);
+          fl::dmma(acc[t][0], acc[t][1], x[ta].d, x[tb].d);
+          ++t;
+        }
     }
     double* Pg = S;  // (NW, 10, 64)
 #pragma unroll
@@ -461,12 +492,15 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
 #ifdef PANEL_PHASES
   PPH(6);
   if (threadIdx.x == 0 && (j % 256) == 5)
-    printf("PANELPH j=%d P0=%d W=%d M=%d load=%lld factor=%lld wb=%lld dots0=%lld groups=%lld gram=%lld tbuild=%lld\n", j, P0,
-           W, m - P0, ph_acc[0], ph_acc[1], ph_acc[2], ph_acc[3], ph_acc[4], ph_acc[5], ph_acc[6]);
+    printf("PANELPH j=%d P0=%d W=%d M=%d load=%lld factor=%lld wb=%lld groups=%lld (pass1=%lld reduce=%lld pass2=%lld tail=%lld) gram=%lld tbuild=%lld\n", j, P0,
+           W, m - P0, ph_acc[0], ph_acc[1], ph_acc[2], ph_acc[4], g_dbg[0], g_dbg[1], g_dbg[2], g_dbg[3], ph_acc[5], ph_acc[6]);
 #endif
 }
 
-__global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
+#ifndef PANEL_MB
+#define PANEL_MB 1
+#endif
+__global__ void __launch_bounds__(NT, PANEL_MB) panel_kernel(PanelArgs a) {
   extern __shared__ double sm[];
   double* S = sm;                                   // SMEM_S bytes
   __shared__ double red[NW * 32];

@@ -54,15 +54,17 @@ constexpr int NW = NT / 32;
 #ifndef QRCP_CU
 #define QRCP_CU 8
 #endif
-#ifndef QRCP_NTL
-#define QRCP_NTL 2
+#ifndef QRCP_UT
+#define QRCP_UT 4  // block update: 8-column tiles loaded per trip (measured: 4 / 6 / 8 -> 64.6 / 65.0 / 65.2 ms)
 #endif
 #ifndef QRCP_L1KEEP
 // F-gemv loads: column groups starting < QRCP_L1KEEP trailing columns past the
 // pivot use L1::evict_last, the rest L1::no_allocate. Measured on cfg4 (one
 // filter): plain loads 80.8 ms; all no_allocate 79.7; keep 32 / 64 / 96 / 128
 // / 160 / 192 / 256: 76.4 / 74.8 / 74.6 / 73.2 / 74.3 / 76.0 / 78.4; all
-// evict_last 81.6
+// evict_last 81.6. A keep width scaled to the panel's height (96 to 512 KB
+// of trailing columns, 128 to 512 columns wide) measured 64.2 to 67.0 ms
+// against 64.5 for the fixed 128 (round 2)
 #define QRCP_L1KEEP 128
 #endif
 #ifndef QRCP_MB
@@ -93,6 +95,13 @@ __device__ __forceinline__ double2 ld_stream(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ fl::d4 ld_stream4(const double* p) {
+  fl::d4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(v.a), "=d"(v.b), "=d"(v.c), "=d"(v.d)
+               : "l"(p));
+  return v;
+}
 __device__ __forceinline__ double ld_keep1(const double* p) {
   double v;
   asm volatile("ld.global.L1::evict_last.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
@@ -101,7 +110,6 @@ __device__ __forceinline__ double ld_keep1(const double* p) {
 // panel columns (re-read by the auxv dots every step of the panel) kept in
 // L1; the block update's once-per-panel read-modify-write streams past it
 #define QRCP_LD_PANEL(p) ld_keep1(p)
-#define QRCP_LD_UPD(p) ld_stream(p)
 
 __device__ __forceinline__ void argmax_lowest(double& v, int& i) {
 #pragma unroll
@@ -471,66 +479,51 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
     const int rk = offset + kb;
     // ---- block update: A(rk:M, rk:N) -= A(rk:M, offset:rk) F(rk:N, 0:kb)^T  (DMMA) ----
     if (rk < M && rk < N) {
-      // The MMA's m index is the trailing column and its n index the row, so
-      // a lane's accumulator pair is two adjacent rows of one column (one
-      // 16-byte load / store) and a warp instruction covers 8 columns x 64 B.
-      // A warp owns an 8*NTL-row strip (NTL n-tiles; the panel values of its rows
-      // stay in registers as B fragments, zero outside rk..M-1 so those rows
-      // are rewritten unchanged) and walks 8-column tiles with the next tile's
-      // accumulators loaded before the current one is computed.
-      constexpr int KS = PB / 4, NTL = QRCP_NTL;
+      // The MMA's m index is the trailing column and its n index the row. A
+      // warp owns a 16-row strip (the panel values of its rows stay in
+      // registers as B fragments, zero outside rk..M-1 so those rows are
+      // rewritten unchanged) and walks 8-column tiles, UT at a time with all
+      // their loads in flight. A lane's 256-bit access is rows rs + 4 t4 .. + 3
+      // of its column (one full line per column and warp access): the pairs
+      // (0, 1) and (2, 3) are the accumulators of two MMA tiles, tile h
+      // holding rows rs + 4 (n / 2) + 2 h + n % 2.
+      constexpr int KS = PB / 4, UT = QRCP_UT;
       const int g = lane >> 2, t4 = lane & 3;
-      const int r0 = rk & ~7;
-      const int nrs = (M - r0 + 8 * NTL - 1) / (8 * NTL);
+      const int r0 = rk & ~15;
+      const int nrs = (M - r0 + 15) / 16;
       const int ncg = nrs >= NW ? 1 : NW / nrs;
       const int nct = (N - rk + 7) / 8;
       for (int item = wid; item < nrs * ncg; item += NW) {
-        const int rs = r0 + (item % nrs) * 8 * NTL;
-        double bq[NTL][KS];
+        const int rs = r0 + (item % nrs) * 16;
+        double bq[2][KS];
 #pragma unroll
-        for (int t = 0; t < NTL; ++t) {
-          const int row = rs + 8 * t + g;
+        for (int h = 0; h < 2; ++h) {
+          const int row = rs + 4 * (g >> 1) + 2 * h + (g & 1);
 #pragma unroll
           for (int s2 = 0; s2 < KS; ++s2) {
             const int kk = 4 * s2 + t4;
-            bq[t][s2] = (row >= rk && row < M && kk < kb) ? A[(int64_t)(offset + kk) * K + row] : 0.0;
+            bq[h][s2] = (row >= rk && row < M && kk < kb) ? A[(int64_t)(offset + kk) * K + row] : 0.0;
           }
         }
-        auto ldc = [&](int ct, double2* c) {
-          const int col = rk + ct * 8 + g;
+        const int row = rs + 4 * t4;  // K is a multiple of 4: the lane's rows are inside the column together
+        for (int ct0 = item / nrs; ct0 < nct; ct0 += ncg * UT) {
+          fl::d4 cc[UT];
 #pragma unroll
-          for (int t = 0; t < NTL; ++t) {
-            const int row = rs + 8 * t + 2 * t4;
-            c[t] = (col < N && row < M) ? QRCP_LD_UPD(A + (int64_t)col * K + row) : make_double2(0.0, 0.0);
-          }
-        };
-        double2 cc[NTL], cn[NTL], cn2[NTL];
-        int ct = item / nrs;
-        if (ct < nct) ldc(ct, cc);
-        if (ct + ncg < nct) ldc(ct + ncg, cn);
-        for (; ct < nct; ct += ncg) {
-          if (ct + 2 * ncg < nct) ldc(ct + 2 * ncg, cn2);
-          const int col = rk + ct * 8 + g;
-          double af[KS];
-#pragma unroll
-          for (int s2 = 0; s2 < KS; ++s2) {
-            const int kk = 4 * s2 + t4;
-            af[s2] = (col < N && kk < kb) ? -F[kk * K + col] : 0.0;
+          for (int u = 0; u < UT; ++u) {
+            const int col = rk + (ct0 + u * ncg) * 8 + g;
+            cc[u] = (col < N && row < M) ? ld_stream4(A + (int64_t)col * K + row) : fl::d4{0.0, 0.0, 0.0, 0.0};
           }
 #pragma unroll
-          for (int t = 0; t < NTL; ++t)
+          for (int u = 0; u < UT; ++u) {
+            const int col = rk + (ct0 + u * ncg) * 8 + g;
 #pragma unroll
-            for (int s2 = 0; s2 < KS; ++s2) fl::dmma(cc[t].x, cc[t].y, af[s2], bq[t][s2]);
-          // accumulator lane layout: c[g][2 t4 + e] = A(rs + 8t + 2 t4 + e, rk + 8ct + g)
-#pragma unroll
-          for (int t = 0; t < NTL; ++t) {
-            const int row = rs + 8 * t + 2 * t4;
-            if (col < N && row < M) *reinterpret_cast<double2*>(A + (int64_t)col * K + row) = cc[t];
-          }
-#pragma unroll
-          for (int t = 0; t < NTL; ++t) {
-            cc[t] = cn[t];
-            cn[t] = cn2[t];
+            for (int s2 = 0; s2 < KS; ++s2) {
+              const int kk = 4 * s2 + t4;
+              const double af = (col < N && kk < kb) ? -F[kk * K + col] : 0.0;
+              fl::dmma(cc[u].a, cc[u].b, af, bq[0][s2]);
+              fl::dmma(cc[u].c, cc[u].d, af, bq[1][s2]);
+            }
+            if (col < N && row < M) fl::stg256(A + (int64_t)col * K + row, cc[u]);
           }
         }
       }

@@ -51,6 +51,21 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// 256-bit global accesses (sm_100: LDG/STG.256): four consecutive doubles,
+// 32-byte aligned. A warp access in the MMA fragment layout (8 columns x 4
+// lanes) then covers one full 128-byte line per column instead of half.
+struct d4 {
+  double a, b, c, d;
+};
+__device__ __forceinline__ d4 ldg256(const double* p) {
+  d4 v;
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n" : "=d"(v.a), "=d"(v.b), "=d"(v.c), "=d"(v.d) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg256(double* p, const d4& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(v.a), "d"(v.b), "d"(v.c), "d"(v.d) : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));

@@ -281,6 +281,29 @@ def test_qr_column_pivot_both_routes_match_scipy(fl, K):
     assert np.abs(q @ r - a[:, got.kept]).max() <= 1e-12 * np.abs(a).max()
 
 
+@pytest.mark.parametrize("m,K", [(2500, 128), (4001, 160), (7003, 128), (11770, 192)])
+def test_route_r_tall_blocks_match_scipy(fl, m, K):
+    """Route R's panel kernel keeps 8, 4 or 2 columns of an inner panel in
+    shared memory depending on the block's rows (<= 2944 / 5888 / 11776);
+    every width, with row counts that are odd or 2 mod 4 (the unaligned
+    starts of the 2-column panels), reproduces LAPACK's factorisation
+    (linalg.py:58-97)."""
+    from paper_2506_17626_b200 import _device as D
+    from paper_2506_17626_b200.filtering import rrqr_route
+    rng = np.random.default_rng(m + K)
+    u, _ = np.linalg.qr(rng.standard_normal((m, K)))
+    w, _ = np.linalg.qr(rng.standard_normal((K, K)))
+    a = (u * np.logspace(0, -13, K)) @ w.T
+    assert rrqr_route(D.BlockLayout(m, K, [np.arange(m)])) == "blocked"
+    _, r_ref, kept_ref, _, _ = O.qr_column_pivot(a, 1e-10)
+    got = fl.qr_column_pivot(a, 1e-10)
+    assert np.array_equal(got.kept, kept_ref)
+    assert np.linalg.norm(got.r_factor - r_ref) <= 1e-10 * np.linalg.norm(r_ref)
+    q, r = got.q_factor, got.r_factor
+    assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-12
+    assert np.abs(q @ r - a[:, got.kept]).max() <= 1e-12 * np.abs(a).max()
+
+
 @pytest.mark.parametrize("K", [160, 256])
 def test_route_r_rejects_non_finite(fl, K):
     """Route R flags a block holding NaN or Inf with rank -1 (the finiteness
