@@ -90,15 +90,10 @@ __device__ __forceinline__ void activation(int act, double pre, double& tv, doub
   }
 }
 
-#ifndef ASM_MINB
-#define ASM_MINB 3
-#endif
+constexpr int ASM_MINB = 3;   // CTAs per SM (D = 3: one less)
 constexpr int CK = 64;        // columns per chunk
 constexpr int TLMAX = 96;     // lattice coordinates per chunk table (sum over axes)
-#ifndef ASM_RPT
-#define ASM_RPT 2
-#endif
-constexpr int RPT = ASM_RPT;  // adjacent rows per thread (16-byte stores)
+constexpr int RPT = 2;        // adjacent rows per thread (16-byte stores)
 static_assert(RPT % 2 == 0, "rows are stored in pairs");
 constexpr int TILE = NT * RPT;
 // |2 (x~ W + b)| bound of one table factor: a product of D <= 3 factors

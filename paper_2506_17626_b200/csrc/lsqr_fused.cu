@@ -38,9 +38,7 @@
 
 #include "common.cuh"
 
-#ifndef ROW_CTAS_PER_SM
-#define ROW_CTAS_PER_SM 3
-#endif
+constexpr int ROW_CTAS_PER_SM = 3;
 // Measured and removed (DESIGN.md §3 K4): an L2 evict_first policy on the Q
 // stream (1.444 vs 1.423 ms per iteration on cfg4) and an evict_last policy
 // on the partial-product stores (1.416 vs 1.399 ms).
@@ -53,9 +51,6 @@ constexpr int smem_per_cta(int mb) { return mb <= 1 ? 232448 : (233472 - mb * 10
 
 __device__ __forceinline__ bool is_done(const fl_lsqr_state* st) { return *(volatile const int32_t*)&st->done; }
 
-#ifndef FL_PDL
-#define FL_PDL 1
-#endif
 // Programmatic dependent launch: the row and fused kernels of an iteration
 // are launched with programmatic stream serialization, trigger their
 // successor's launch on entry and wait for their predecessor's completion
@@ -66,10 +61,8 @@ __device__ __forceinline__ bool is_done(const fl_lsqr_state* st) { return *(vola
 // 0.1378 / 0.1360 / 0.1353 / 0.1348, cfg2 0.0430 / 0.0410 / 0.0410 / 0.0397:
 // a launch-latency win for the small configs, neutral at cfg4.
 __device__ __forceinline__ void pdl_enter() {
-#if FL_PDL
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-#endif
 }
 
 template <typename... KArgs, typename... Args>
@@ -82,7 +75,7 @@ cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, si
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (FL_PDL && pdl) ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);

@@ -20,18 +20,12 @@
 namespace {
 
 constexpr int NB = 32;
-#ifndef PANEL_NT
-// measured on cfg4: 512 threads 2.11 ms per launch, 384 threads (160
-// registers) 2.34 ms
-#define PANEL_NT 512
-#endif
-constexpr int NT = PANEL_NT;
+// measured on cfg4 (round-1 kernel): 512 threads 2.11 ms per launch, 384
+// threads (160 registers) 2.34 ms
+constexpr int NT = 512;
 constexpr int NW = NT / 32;
 // (measured on cfg4: 184 KB 2.09 ms per launch, 164 KB 2.14, 132 KB (W = 4) 2.50)
-#ifndef PANEL_SMEM_KB
-#define PANEL_SMEM_KB 184
-#endif
-constexpr int SMEM_S = PANEL_SMEM_KB * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
+constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
 // (measured: 256 threads at two CTAs per SM, 84 KB panels, was slower: 2.80 vs 2.25 ms per launch)
 
 // Sum N (a power of two <= 32) per-thread partials across the CTA; results
@@ -221,9 +215,9 @@ __shared__ long long g_dbg[4];
 #define APH(n, t0)
 #endif
 
-#ifndef PANEL_LD
-#define PANEL_LD 6
-#endif
+// 256-bit loads in flight per lane and trip (measured on cfg4, 16-byte loads:
+// 8 / 12 / 16 / 18 in flight 1.25 / 1.26 / 1.29 / 1.31 ms per launch)
+constexpr int PANEL_LD = 6;
 
 template <int W, int NT8>
 __device__ void apply_rest(const double* S, int Mq, const double* Tw, const double* Xj, double* Aj, int64_t ld, int c,
@@ -497,10 +491,7 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
 #endif
 }
 
-#ifndef PANEL_MB
-#define PANEL_MB 1
-#endif
-__global__ void __launch_bounds__(NT, PANEL_MB) panel_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
   extern __shared__ double sm[];
   double* S = sm;                                   // SMEM_S bytes
   __shared__ double red[NW * 32];

@@ -34,20 +34,10 @@ constexpr int TN = 64;    // C columns per CTA
 // extra KB of shared memory is taken from L1, which this kernel needs). Without the per-chunk
 // barriers (incorrect, timing only) 72 ms: the barriers, not the loads or
 // shared-memory bandwidth, hold the DMMA pipe near 68% busy.
-#ifndef QF_NW
-#define QF_NW 16
-#endif
-#ifndef QF_MINB
-#define QF_MINB 1
-#endif
-#ifndef QF_STAGES
-#define QF_STAGES 3
-#endif
+constexpr int QF_NW = 16, QF_MINB = 1, QF_STAGES = 3;
 constexpr int NW = QF_NW, NT = NW * 32;
 constexpr int RC = 2 * NW;  // rows per staged chunk
-#ifndef QF_PAD
-#define QF_PAD 4
-#endif
+constexpr int QF_PAD = 4;
 constexpr int LDS = RC + QF_PAD; // 4: = 4 mod 16, conflict-free 8-byte fragment loads
 // (measured on cfg4: pad 4 78.2 ms, pad 2 — 2-way conflicts, ring small enough
 // for the 164 KB shared-memory configuration — 80.4, pad 0 128 ms)

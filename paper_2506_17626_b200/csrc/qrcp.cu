@@ -40,24 +40,13 @@
 
 namespace {
 
-#ifndef QRCP_NT
 // measured on cfg4 (ncu, one filter): 256 threads x 2 CTAs/SM 89.0 ms;
 // one CTA/SM: 384 threads 80.8 ms (166 registers), 512 81.6, 448 106.7,
 // 320 129.6, 640 117.3; 512 with a 32-column panel 92.3 (spills)
-#define QRCP_NT 384
-#endif
-constexpr int NT = QRCP_NT;
+constexpr int NT = 384;
 constexpr int NW = NT / 32;
-#ifndef QRCP_PB
-#define QRCP_PB 16
-#endif
-#ifndef QRCP_CU
-#define QRCP_CU 8
-#endif
-#ifndef QRCP_UT
-#define QRCP_UT 4  // block update: 8-column tiles loaded per trip (measured: 4 / 6 / 8 -> 64.6 / 65.0 / 65.2 ms)
-#endif
-#ifndef QRCP_L1KEEP
+constexpr int QRCP_CU = 8;  // gemv: columns in flight per warp
+constexpr int QRCP_UT = 4;  // block update: 8-column tiles loaded per trip (measured: 4 / 6 / 8 -> 64.6 / 65.0 / 65.2 ms)
 // F-gemv loads: column groups starting < QRCP_L1KEEP trailing columns past the
 // pivot use L1::evict_last, the rest L1::no_allocate. Measured on cfg4 (one
 // filter): plain loads 80.8 ms; all no_allocate 79.7; keep 32 / 64 / 96 / 128
@@ -65,12 +54,9 @@ constexpr int NW = NT / 32;
 // evict_last 81.6. A keep width scaled to the panel's height (96 to 512 KB
 // of trailing columns, 128 to 512 columns wide) measured 64.2 to 67.0 ms
 // against 64.5 for the fixed 128 (round 2)
-#define QRCP_L1KEEP 128
-#endif
-#ifndef QRCP_MB
-#define QRCP_MB 1
-#endif
-constexpr int PB = QRCP_PB;  // panel width (F has PB columns)
+constexpr int QRCP_L1KEEP = 128;
+constexpr int QRCP_MB = 1;
+constexpr int PB = 16;  // panel width (F has PB columns)
 
 struct QrcpArgs {
   double* R0;          // (J, K, K) column-major, ld K; on exit: R above, reflectors below
@@ -357,10 +343,8 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
               for (int u = 0; u < CU; ++u) d[u] += x[u].x * v0 + x[u].y * v1 + y[u].x * w0 + y[u].y * w1;
             }
           };
-#ifndef QRCP_DIAG_NOGEMV  // diagnostic timing build only: gemv loads skipped, F = 0 (wrong results)
           if (c0 < QRCP_L1KEEP) rows_loop(std::true_type{});
           else rows_loop(std::false_type{});
-#endif
           {
             const double s = fl::warp_multi_sum<CU>(d);  // lane l: column u = l / (32 / CU)
             const int u = lane / (32 / CU);

@@ -16,16 +16,12 @@ namespace {
 
 constexpr int TN = 64;            // C columns per CTA
 constexpr int RC = 32;            // rows per staged chunk
-#ifndef WY_T_SMEM
-#define WY_T_SMEM 0  // 1: T_j staged in shared memory. Measured on cfg4 (wy<64>, 2 filters): staged 79.8 ms, read through L1/L2 75.3 (the 32 KB go to L1)
-#endif
-#ifndef WY_STAGES64
-#define WY_STAGES64 4  // measured on cfg4: 1.4% faster than 3 (296.9 vs 301.1 ms per two filters)
-#endif
-// (measured on cfg4, wy<32>, 2 filters: 3 stages 30.3 ms, 2 stages 38.8, 4 stages 42.3)
-#ifndef WY_STAGES32
-#define WY_STAGES32 3
-#endif
+// T_j is read through L1/L2, not staged in shared memory (measured on cfg4,
+// wy<64>, 2 filters: staged 79.8 ms, through L1/L2 75.3: the 32 KB go to L1).
+// Ring stages, measured on cfg4: wy<64> 4 stages 1.4% faster than 3 (296.9 vs
+// 301.1 ms per two filters); wy<32>, 2 filters: 3 stages 30.3 ms, 2 stages
+// 38.8, 4 stages 42.3.
+constexpr int WY_STAGES64 = 4, WY_STAGES32 = 3;
 template <int NB>
 constexpr int stages_for() { return NB == 64 ? WY_STAGES64 : WY_STAGES32; }
 constexpr int LDS = RC + 4;       // padded column length of a staged chunk
@@ -36,7 +32,7 @@ struct Cfg {
   static constexpr int NW = 8 * NB / 32;
   static constexpr int NT = NW * 32;
   static constexpr int STAGES = stages_for<NB>();
-  static constexpr size_t smem = (size_t)(STAGES * NB * LDS + STAGES * TN * LDS + NB * LDW + (WY_T_SMEM ? NB * NB : 0)) * 8;
+  static constexpr size_t smem = (size_t)(STAGES * NB * LDS + STAGES * TN * LDS + NB * LDW) * 8;
 };
 
 template <int NB>
@@ -75,7 +71,6 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
   double* Vs = sm;                            // [STAGES][NB][LDS]
   double* Cs = Vs + STAGES * NB * LDS;        // [STAGES][TN][LDS]
   double* Ws = Cs + STAGES * TN * LDS;        // [NB][LDW]
-  double* Ts = Ws + NB * LDW;                 // [NB][NB] column-major
 
   int j, c0;
   if (a.tiles) {
@@ -96,12 +91,7 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
   const int nchunks = (mj - r0 + RC - 1) / RC;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
 
-#if WY_T_SMEM
-  for (int i = threadIdx.x; i < NB * NB; i += Cfg<NB>::NT) Ts[i] = a.T[(int64_t)j * a.tstride + i];
-#else
   const double* Tg = a.T + (int64_t)j * a.tstride;  // read through L1/L2 in phase 2
-  (void)Ts;
-#endif
 
   auto stage_v = [&](int s) { return Vs + s * NB * LDS; };
   auto stage_c = [&](int s) { return Cs + s * TN * LDS; };
@@ -215,11 +205,7 @@ __global__ void __launch_bounds__(Cfg<NB>::NT, (NB == 32 ? 2 : 1)) wy_apply_kern
 #pragma unroll
     for (int k0 = 0; k0 < NB; k0 += 4) {
       const int ar = mt * 8 + g, ac = k0 + t;
-#if WY_T_SMEM
-      const double av = a.transT ? Ts[ar * NB + ac] : Ts[ac * NB + ar];  // op(T)[ar][ac]
-#else
-      const double av = __ldg(a.transT ? Tg + ar * NB + ac : Tg + ac * NB + ar);
-#endif
+      const double av = __ldg(a.transT ? Tg + ar * NB + ac : Tg + ac * NB + ar);  // op(T)[ar][ac]
 #pragma unroll
       for (int n = 0; n < 4; ++n) fl::dmma(p2[n][0], p2[n][1], av, Ws[(k0 + t) * LDW + (ntb + n) * 8 + g]);
     }
