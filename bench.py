@@ -350,11 +350,9 @@ def product(args, rank, world, local_rank):
         "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8(d) inputs, seeded)",
-        "config": {"workload": f"{args.config}: {wl.description}",
-                   "lsqr_iters_per_solve": iters, "sigma": wl.sigma,
-                   "rows": L.nrows, "cols": int(L.J * L.K), "kept": int(fs.kept_total),
-                   "l2": f"inputs larger than L2 (Q {nnz_q * 8 / 1e9:.2f} GB, A {nnz_a * 8 / 1e9:.2f} GB)",
-                   "parallelism": f"replicas x{world}"},
+        "config": config_of(args, wl, iters, world, int(L.nrows)),
+        "workload_stats": {"kept": int(fs.kept_total), "Q_GB": round(nnz_q * 8 / 1e9, 2),
+                           "A_store_GB": round(nnz_a * 8 / 1e9, 2)},
         "roofline": {"bound": "hbm", "kernel": "LSQR iteration (fused_kernel + row_kernel)",
                      "achieved": round(bytes_it / t_it / 1e9, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(bytes_it / t_it / 1e9 / hbm, 4),
@@ -511,6 +509,18 @@ def _block_rows(wl):
     return m, multi
 
 
+def config_of(args, wl, iters, world, rows):
+    """The workload description both arms print (same keys and values: the
+    driver compares them). Sizes from the host-side block row counts."""
+    m, _ = _block_rows(wl)
+    K = wl.basis.feature_count
+    return {"workload": f"{args.config}: {wl.description}", "lsqr_iters_per_solve": iters,
+            "sigma": wl.sigma, "rows": rows, "cols": int(m.size * K),
+            "l2": f"inputs larger than L2 (A {float(m.sum()) * K * 8 / 1e9:.2f} GB of block entries, "
+                  f"Q of the same order)",
+            "parallelism": f"replicas x{world}"}
+
+
 def ref_sample(wl, iters, per_stratum, seed):
     """featlsq's own stage functions on a stratified block sample of the
     workload, extrapolated to the full solve (module docstring)."""
@@ -592,7 +602,7 @@ def ref_sample(wl, iters, per_stratum, seed):
     solve = (t_glob + asm_full + qr_full + (t1 - t0) * scale_q + iters * t_it
              + (t3 - t2) * J / len(sel))
     return {"value": round(1.0 / solve, 8), "unit": UNIT, "cores": os.cpu_count(),
-            "kind": "reference",
+            "kind": "reference", "rows": int(sysj.row_count),
             "sample": (f"featlsq (baseline/_ref) assemble / filter_system / precondition / lsqr / "
                        f"recover_solution on {len(sel)} of {J} blocks ({per_stratum} per "
                        f"corner/edge/interior stratum, seed {seed}) plus the full lattice, "
@@ -627,8 +637,7 @@ def reference(args, rank, world):
             "ms_per_step": round(1e3 / mid["value"], 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8(d) inputs, seeded)",
-            "config": {"workload": f"{args.config}: {wl.description}",
-                       "lsqr_iters_per_solve": iters, "sigma": wl.sigma},
+            "config": config_of(args, wl, iters, world, int(mid["rows"])),
             "cpu_baseline": {"value": mid["value"], "unit": UNIT, "cores": mid["cores"],
                              "kind": mid["kind"], "sample": mid["sample"]},
             "e2e": {"value": mid["value"], "unit": UNIT, "h2d_bytes_per_step": 0,

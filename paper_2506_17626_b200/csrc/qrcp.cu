@@ -211,9 +211,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       double* ci = A + (int64_t)i * K;
       double* cp = A + (int64_t)p * K;
       double ss = 0.0;  // dlarfg's ||v(i+1:M)||^2, summed as the column is formed
-      for (int r = threadIdx.x; r < M; r += NT) {
-        const double xi = ci[r];
-        double xp = cp[r];
+      auto form_row = [&](int r, double xi, double xp) {
         if (p != i) cp[r] = xi;
         if (r < i) {
           if (p != i) ci[r] = xp;
@@ -229,6 +227,15 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
           if (r > i) ss += xp * xp;
           if (r == i) s_alpha = xp;
         }
+      };
+      // a thread's rows r and r + NT (M <= 2 NT for every K of this route):
+      // both rows' column values are requested before either is used
+      for (int r = threadIdx.x; r < M; r += 2 * NT) {
+        const int r2 = r + NT;
+        const double xi = ci[r], xp = cp[r];
+        const double xi2 = r2 < M ? ci[r2] : 0.0, xp2 = r2 < M ? cp[r2] : 0.0;
+        form_row(r, xi, xp);
+        if (r2 < M) form_row(r2, xi2, xp2);
       }
       ss = fl::warp_sum(ss);
       if (lane == 0) red[wid] = ss;
@@ -270,13 +277,17 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
 #pragma unroll
       for (int w = 0; w < NW; ++w) ss += red[w];
       const double alpha = s_alpha;
-      const double xnorm = sqrt(ss);
+      const bool xzero = ss == 0.0;  // sqrt(ss) == 0 exactly when ss == 0
       double beta, t;
-      if (xnorm == 0.0) {
+      if (xzero) {
         t = 0.0;
         beta = alpha;
       } else {
-        beta = -copysign(hypot(alpha, xnorm), alpha);
+        // ||(alpha, x)|| from the sum of squares with one sqrt on the step's
+        // critical path (dlapy2's scaled form only outside the safe range)
+        const double n2 = fma(alpha, alpha, ss);
+        const double nrm = (n2 > 1e-280 && n2 < 1e280 && ss > 1e-280) ? sqrt(n2) : hypot(alpha, sqrt(ss));
+        beta = -copysign(nrm, alpha);
         t = (beta - alpha) / beta;
       }
       if (i == 0) lead = fabs(beta);
@@ -291,7 +302,7 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       }
       // v = x * scal (dlarfg's dscal), v_i = 1, scaled once in shared memory
       // (one more barrier) and read as is below
-      const double scal = (xnorm == 0.0) ? 1.0 : 1.0 / (alpha - beta);
+      const double scal = xzero ? 1.0 : 1.0 / (alpha - beta);
       for (int r = i + 1 + threadIdx.x; r < M; r += NT) {
         const double x = v[r - i] * scal;
         v[r - i] = x;
@@ -375,12 +386,22 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       // ---- F(:, k) += F(:, 0:k) auxv (F(offset..i, k) = 0 first);
       //      A(i, i+1:N) -= A(i, offset:i+1) F(i+1:N, 0:k+1)^T ; downdate ----
       for (int c = offset + threadIdx.x; c < N; c += NT) {
+        // F(c, 0:k) is read once (all loads in flight), used by both sums in
+        // the same order as the plain loops
+        double fv[PB];
+#pragma unroll
+        for (int kk = 0; kk < PB; ++kk) fv[kk] = (kk < k) ? F[kk * K + c] : 0.0;
         double f = (c <= i) ? 0.0 : F[k * K + c];
-        for (int kk = 0; kk < k; ++kk) f += F[kk * K + c] * auxv[kk];
+#pragma unroll
+        for (int kk = 0; kk < PB; ++kk)
+          if (kk < k) f += fv[kk] * auxv[kk];
         F[k * K + c] = f;
         if (c > i) {
           double x = rowA[c];
-          for (int kk = 0; kk <= k; ++kk) x -= rowi[kk] * F[kk * K + c];
+#pragma unroll
+          for (int kk = 0; kk < PB; ++kk)
+            if (kk < k) x -= rowi[kk] * fv[kk];
+          x -= rowi[k] * f;
           A[(int64_t)c * K + i] = x;
           if (i + 1 < M && vn1[c] != 0.0) {
             double tt = fabs(x) / vn1[c];

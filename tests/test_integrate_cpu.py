@@ -70,6 +70,16 @@ def test_reference_sampler_runs_featlsq_stages():
     assert sd.subdomain_count == 2 and sd.multi_index(1) == wl.dec.multi_index(7)
     assert sd.count_per_dim == wl.dec.count_per_dim
     assert np.array_equal(sd.centers, wl.dec.centers)
+    # both bench arms describe the workload with the same helper: the
+    # reference arm's row count (featlsq's own) is the product arm's
+    ref = featlsq.assembly.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    assert out["rows"] == ref.row_count
+
+    class A:
+        config = "cfg1"
+    cfg = bench.config_of(A, wl, 100, 1, out["rows"])
+    assert set(cfg) == {"workload", "lsqr_iters_per_solve", "sigma", "rows", "cols", "l2", "parallelism"}
+    assert cfg["rows"] == ref.row_count and cfg["cols"] == ref.column_count
 
 
 def test_install_reference_is_git_ignored():
