@@ -386,22 +386,12 @@ __global__ void __launch_bounds__(NT, QRCP_MB) qrcp_kernel(QrcpArgs q) {
       // ---- F(:, k) += F(:, 0:k) auxv (F(offset..i, k) = 0 first);
       //      A(i, i+1:N) -= A(i, offset:i+1) F(i+1:N, 0:k+1)^T ; downdate ----
       for (int c = offset + threadIdx.x; c < N; c += NT) {
-        // F(c, 0:k) is read once (all loads in flight), used by both sums in
-        // the same order as the plain loops
-        double fv[PB];
-#pragma unroll
-        for (int kk = 0; kk < PB; ++kk) fv[kk] = (kk < k) ? F[kk * K + c] : 0.0;
         double f = (c <= i) ? 0.0 : F[k * K + c];
-#pragma unroll
-        for (int kk = 0; kk < PB; ++kk)
-          if (kk < k) f += fv[kk] * auxv[kk];
+        for (int kk = 0; kk < k; ++kk) f += F[kk * K + c] * auxv[kk];
         F[k * K + c] = f;
         if (c > i) {
           double x = rowA[c];
-#pragma unroll
-          for (int kk = 0; kk < PB; ++kk)
-            if (kk < k) x -= rowi[kk] * fv[kk];
-          x -= rowi[k] * f;
+          for (int kk = 0; kk <= k; ++kk) x -= rowi[kk] * F[kk * K + c];
           A[(int64_t)c * K + i] = x;
           if (i + 1 < M && vn1[c] != 0.0) {
             double tt = fabs(x) / vn1[c];
