@@ -156,11 +156,13 @@ int fl_rrqr(const fl_blockop* blocks, int32_t K, int32_t max_rows, double sigma,
  * Q_j = Q0 [Q1; 0]. `A` is left unchanged; Q_j is written to the store `Q`
  * (same layout as A). `workspace` needs fl_rrqr_blocked_workspace() bytes;
  * store_elems = total doubles of the A store. No host synchronisation.
- * Shared-memory bounds: K <= FL_RRQR_BLOCKED_MAX_K and max_rows <=
- * FL_RRQR_BLOCKED_MAX_ROWS (else FL_ERR_INVALID). fl_rrqr stages one
+ * Shared-memory bound: K <= FL_RRQR_BLOCKED_MAX_K (else FL_ERR_INVALID); any
+ * number of rows (blocks of up to FL_RRQR_BLOCKED_MAX_ROWS rows have the
+ * inner panels of K2a staged in shared memory, taller ones are factored in
+ * place: slower, same results). fl_rrqr stages one
  * max_rows-long reflector on chip: 8 * (4 K + max_rows) + 4 K bytes <= 220 KB
  * (about 25.8k rows at K = 512), else FL_ERR_INVALID; the host maps blocks
- * beyond both bounds to CapExceededError. */
+ * that neither route takes to CapExceededError. */
 #define FL_RRQR_BLOCKED_MAX_K 640
 #define FL_RRQR_BLOCKED_MAX_ROWS 11776
 #define FL_RRQR_DIRECT_SMEM_MAX (220 * 1024)

@@ -76,8 +76,10 @@ struct PanelArgs {
 };
 
 template <int W>
-__device__ void factor_inner(double* S, int Mq, double* red, double* sc, double* Tw, double* tau_j, int col0) {
-  // S: W columns of Mq rows (column-major, stride Mq), rows relative to col0.
+__device__ void factor_inner(double* S, int Mq, int64_t sq, double* red, double* sc, double* Tw, double* tau_j,
+                             int col0) {
+  // S: W columns of Mq rows (column-major, stride sq: shared memory, or the
+  // block itself in place for blocks too tall to stage), rows relative to col0.
   // One pass over the rows per column: the pass that applies H_s to the
   // columns right of s also accumulates, for column s+1, its squared norm
   // and its UNSCALED dots x^T S[k] with the columns right of it and with the
@@ -89,17 +91,17 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
   __shared__ double rowb[2][W];
   double acc[2 * W];
   auto accumulate = [&](int s1, int r) {  // rows r > s1 of column s1 (updated)
-    const double x = S[s1 * Mq + r];
+    const double x = S[s1 * sq + r];
     acc[0] += x * x;
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-      if (k > s1) acc[k] += x * S[k * Mq + r];
-      if (k < s1) acc[W + k] += x * S[k * Mq + r];  // reflector k (r > s1 > k: stored)
+      if (k > s1) acc[k] += x * S[k * sq + r];
+      if (k < s1) acc[W + k] += x * S[k * sq + r];  // reflector k (r > s1 > k: stored)
     }
   };
   auto stash = [&](int s1) {  // row s1 of every column, by its owner
 #pragma unroll
-    for (int k = 0; k < W; ++k) rowb[s1 & 1][k] = S[k * Mq + s1];
+    for (int k = 0; k < W; ++k) rowb[s1 & 1][k] = S[k * sq + s1];
   };
 #pragma unroll
   for (int k = 0; k < 2 * W; ++k) acc[k] = 0.0;
@@ -150,19 +152,19 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
       if (r < s) continue;
       double x[W];  // row r: reflector entries (k < s), then columns s..W-1
 #pragma unroll
-      for (int k = 0; k < W; ++k) x[k] = S[k * Mq + r];
+      for (int k = 0; k < W; ++k) x[k] = S[k * sq + r];
       double v = 1.0;
       if (r == s) {
-        S[s * Mq + s] = beta;
+        S[s * sq + s] = beta;
       } else {
         v = x[s] * scal;
-        S[s * Mq + r] = v;
+        S[s * sq + r] = v;
       }
 #pragma unroll
       for (int k = 0; k < W; ++k) {
         if (k > s) {
           if (t != 0.0) x[k] = fma(-pk[k], v, x[k]);
-          S[k * Mq + r] = x[k];
+          S[k * sq + r] = x[k];
         } else if (k == s) {
           x[k] = v;
         }
@@ -190,10 +192,10 @@ __device__ void factor_inner(double* S, int Mq, double* red, double* sc, double*
 }
 
 // entry (r, k) of the resident inner panel's V: unit lower trapezoidal, W
-// columns of Mq rows in S (stride Mq); zero outside
+// columns of Mq rows in S (stride sq); zero outside
 template <int W>
-__device__ __forceinline__ double vval(const double* S, int Mq, int r, int k) {
-  return (k >= W || r >= Mq || r < k) ? 0.0 : (r == k ? 1.0 : S[k * Mq + r]);
+__device__ __forceinline__ double vval(const double* S, int64_t sq, int Mq, int r, int k) {
+  return (k >= W || r >= Mq || r < k) ? 0.0 : (r == k ? 1.0 : S[k * sq + r]);
 }
 
 // X -= V (Tw^T (V^T X)) for the nrest (<= 8 NT8) panel columns X right of the
@@ -220,7 +222,7 @@ __shared__ long long g_dbg[4];
 constexpr int PANEL_LD = 6;
 
 template <int W, int NT8>
-__device__ void apply_rest(const double* S, int Mq, const double* Tw, const double* Xj, double* Aj, int64_t ld, int c,
+__device__ void apply_rest(const double* S, int64_t sq, int Mq, const double* Tw, const double* Xj, double* Aj, int64_t ld, int c,
                            int nrest, double* Pw, double* Zs) {
   constexpr int UN = PANEL_LD / NT8 > 0 ? PANEL_LD / NT8 : 1;  // ~PANEL_LD 256-bit loads in flight per lane
   constexpr int PC = 8 * NT8;                                  // padded column count
@@ -267,8 +269,8 @@ __device__ void apply_rest(const double* S, int Mq, const double* Tw, const doub
 #pragma unroll
       for (int u = 0; u < UN; ++u) {
         const int r = (ch0 + u) * 16 + 4 * t4 - rsh;
-        const double v0 = vval<W>(S, Mq, r, g), v1 = vval<W>(S, Mq, r + 1, g);
-        const double v2 = vval<W>(S, Mq, r + 2, g), v3 = vval<W>(S, Mq, r + 3, g);
+        const double v0 = vval<W>(S, sq, Mq, r, g), v1 = vval<W>(S, sq, Mq, r + 1, g);
+        const double v2 = vval<W>(S, sq, Mq, r + 2, g), v3 = vval<W>(S, sq, Mq, r + 3, g);
 #pragma unroll
         for (int t = 0; t < NT8; ++t) {
           fl::dmma(acc[t][0], acc[t][1], v0, x[u][t].a);
@@ -318,7 +320,7 @@ __device__ void apply_rest(const double* S, int Mq, const double* Tw, const doub
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int s2 = 0; s2 < KS; ++s2) vb[h][s2] = vval<W>(S, Mq, rb + 2 * h, t4 + 4 * s2);
+        for (int s2 = 0; s2 < KS; ++s2) vb[h][s2] = vval<W>(S, sq, Mq, rb + 2 * h, t4 + 4 * s2);
       const int r = (ch0 + u) * 16 + 4 * t4 - rsh;
 #pragma unroll
       for (int t = 0; t < NT8; ++t) {
@@ -349,7 +351,10 @@ __device__ void apply_rest(const double* S, int Mq, const double* Tw, const doub
 #define PPH(n)
 #endif
 
-template <int W>
+// INPLACE: the inner panels are factored where they lie in the block (blocks
+// too tall for even two staged columns): same passes, global instead of
+// shared accesses, each thread re-reading only rows it wrote itself.
+template <int W, bool INPLACE>
 __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, double* sc, double* Tw,
                            double* Gs, double* Pw, double* Zs) {
   const int m = a.m[j];
@@ -367,30 +372,39 @@ __device__ void panel_body(const PanelArgs& a, int j, double* S, double* red, do
     const int Mq = m - c;
     // columns right of the first inner panel are first read from src, later from A
     const double* Xj = (q == 0 && a.src) ? a.src + a.off[j] : Aj;
-    // load inner panel rows c..m-1 (8-byte cp.async: every load in flight at once)
-    for (int k = 0; k < W; ++k)
+    double* Sp = INPLACE ? Aj + (int64_t)c * ld + c : S;  // the inner panel's columns, rows from c
+    const int64_t sq = INPLACE ? ld : Mq;
+    if (INPLACE) {
+      if (Xj != Aj)
+        for (int k = 0; k < W; ++k)
+          for (int r = threadIdx.x; r < Mq; r += NT) Sp[k * sq + r] = Xj[(int64_t)(c + k) * ld + c + r];
+    } else {
+      // load inner panel rows c..m-1 (8-byte cp.async: every load in flight at once)
+      for (int k = 0; k < W; ++k)
 #pragma unroll 2
-      for (int r = threadIdx.x; r < Mq; r += NT) {
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(S + k * Mq + r);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(Xj + (int64_t)(c + k) * ld + c + r)
-                     : "memory");
-      }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
+        for (int r = threadIdx.x; r < Mq; r += NT) {
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(S + k * Mq + r);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(Xj + (int64_t)(c + k) * ld + c + r)
+                       : "memory");
+        }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
     __syncthreads();
     PPH(0);
-    factor_inner<W>(S, Mq, red, sc, Tw, tau_j, c);
+    factor_inner<W>(Sp, Mq, sq, red, sc, Tw, tau_j, c);
     PPH(1);
-    for (int k = 0; k < W; ++k)
-      for (int r = threadIdx.x; r < Mq; r += NT) Aj[(int64_t)(c + k) * ld + c + r] = S[k * Mq + r];
+    if (!INPLACE)
+      for (int k = 0; k < W; ++k)
+        for (int r = threadIdx.x; r < Mq; r += NT) Aj[(int64_t)(c + k) * ld + c + r] = S[k * Mq + r];
     PPH(2);
     // apply (I - V Tw V^T)^T to the panel columns right of this inner panel
     {
       const int nrest = P0 + NB - (c + W);
       const int nt8 = (nrest + 7) / 8;
-      if (nt8 == 4) apply_rest<W, 4>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
-      else if (nt8 == 3) apply_rest<W, 3>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
-      else if (nt8 == 2) apply_rest<W, 2>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
-      else if (nt8 == 1) apply_rest<W, 1>(S, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      if (nt8 == 4) apply_rest<W, 4>(Sp, sq, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      else if (nt8 == 3) apply_rest<W, 3>(Sp, sq, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      else if (nt8 == 2) apply_rest<W, 2>(Sp, sq, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
+      else if (nt8 == 1) apply_rest<W, 1>(Sp, sq, Mq, Tw, Xj, Aj, ld, c, nrest, Pw, Zs);
       PPH(4);
     }
   }
@@ -504,10 +518,10 @@ __global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
   const int M = a.m[j] - a.P0;
   if (M <= 0) return;
   const int cap = SMEM_S / 8;
-  if (8 * M <= cap) panel_body<8>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
-  else if (4 * M <= cap) panel_body<4>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
-  else if (2 * M <= cap) panel_body<2>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
-  else __trap();  // excluded by rrqr_route (filtering.py BLOCKED_MAX_ROWS) and panel_factor
+  if (8 * M <= cap) panel_body<8, false>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
+  else if (4 * M <= cap) panel_body<4, false>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
+  else if (2 * M <= cap) panel_body<2, false>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
+  else panel_body<8, true>(a, j, S, red, sc, Tw, Gs, Pw, Zs);  // taller than FL_RRQR_BLOCKED_MAX_ROWS
 }
 
 }  // namespace

@@ -80,33 +80,39 @@ __global__ void __launch_bounds__(NT) gather_kernel(fl_blockop op, double* __res
 
 // -------------------------------------------------------------- transposed
 // out[col_off_j + c] = B_j[:, c] . rs, rs = r[rows_j] (optionally scaled).
+// The first ns rows of rs are staged in shared memory (all m of them unless
+// the block is taller than the staging buffer); rows past ns are gathered
+// from src[rows[i]] / div as they are used.
 __device__ __forceinline__ double col_dot(const double* __restrict__ col, int m, const double* __restrict__ rs,
-                                          int lane) {
+                                          int lane, int ns, const double* __restrict__ src,
+                                          const int32_t* __restrict__ rows, double div) {
+  const int ms = m < ns ? m : ns;
   double a0 = 0.0, a1 = 0.0;
   int i = lane;
-  for (; i + 32 < m; i += 64) {
+  for (; i + 32 < ms; i += 64) {
     a0 += __ldg(col + i) * rs[i];
     a1 += __ldg(col + i + 32) * rs[i + 32];
   }
-  if (i < m) a0 += __ldg(col + i) * rs[i];
+  if (i < ms) a0 += __ldg(col + i) * rs[i];
+  for (i = ms + lane; i < m; i += 32) a0 += __ldg(col + i) * (src[rows[i]] / div);
   return fl::warp_sum(a0 + a1);
 }
 
 __global__ void __launch_bounds__(NT) adj_kernel(fl_blockop op, const double* __restrict__ r,
-                                                 double* __restrict__ out) {
+                                                 double* __restrict__ out, int ns) {
   extern __shared__ double rs[];
   const int j = op.col_tiles[2 * blockIdx.x];
   const int c0 = op.col_tiles[2 * blockIdx.x + 1];
   const int m = op.m[j];
   const int32_t* rows = op.rows + op.row_off[j];
-  for (int i = threadIdx.x; i < m; i += NT) rs[i] = r[rows[i]];
+  for (int i = threadIdx.x; i < m && i < ns; i += NT) rs[i] = r[rows[i]];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nc = op.ncols[j];
   const double* Bj = op.vals + op.off[j];
   const int64_t ld = op.ld[j];
   for (int c = c0 + wid; c < c0 + CT && c < nc; c += NW) {
-    double d = col_dot(Bj + c * ld, m, rs, lane);
+    double d = col_dot(Bj + c * ld, m, rs, lane, ns, r, rows, 1.0);
     if (lane == 0) out[op.col_off[j] + c] = d;
   }
 }
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(NT) lsqr_ured_kernel(fl_blockop op, fl_lsqr_ve
 }
 
 __global__ void __launch_bounds__(NT) lsqr_qtu_kernel(fl_blockop op, fl_lsqr_vecs vec, fl_lsqr_state* st,
-                                                      int64_t it) {
+                                                      int64_t it, int ns) {
   if (state_done(st)) return;
   extern __shared__ double rs[];
   __shared__ double sh[NW];
@@ -213,12 +219,12 @@ __global__ void __launch_bounds__(NT) lsqr_qtu_kernel(fl_blockop op, fl_lsqr_vec
   double ass = 0.0;
   if (beta > 0.0) {
     const int32_t* rows = op.rows + op.row_off[j];
-    for (int i = threadIdx.x; i < m; i += NT) rs[i] = vec.u[rows[i]] / beta;  // u = u / beta (:123)
+    for (int i = threadIdx.x; i < m && i < ns; i += NT) rs[i] = vec.u[rows[i]] / beta;  // u = u / beta (:123)
     __syncthreads();
     const double* Bj = op.vals + op.off[j];
     const int64_t ld = op.ld[j];
     for (int c = c0 + wid; c < c0 + CT && c < nc; c += NW) {
-      const double d = col_dot(Bj + c * ld, m, rs, lane);
+      const double d = col_dot(Bj + c * ld, m, rs, lane, ns, vec.u, rows, beta);
       if (lane == 0) {
         const double vn = d - beta * vec.v[co + c];  // v' = Q^T u - beta v (:136)
         vec.vp[co + c] = vn;
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(NT) lsqr_init_a(fl_blockop op, const double* _
 }
 
 // init: v' = Q^T (rhs/beta), alpha = ||v'|| (solvers.py:108-117); x = w = 0
-__global__ void __launch_bounds__(NT) lsqr_init_b(fl_blockop op, fl_lsqr_vecs vec, fl_lsqr_state* st) {
+__global__ void __launch_bounds__(NT) lsqr_init_b(fl_blockop op, fl_lsqr_vecs vec, fl_lsqr_state* st, int ns) {
   if (state_done(st)) return;
   extern __shared__ double rs[];
   __shared__ double sh[NW];
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(NT) lsqr_init_b(fl_blockop op, fl_lsqr_vecs ve
   const int64_t co = op.col_off[j];
   const double beta = st->beta;
   const int32_t* rows = op.rows + op.row_off[j];
-  for (int i = threadIdx.x; i < m; i += NT) rs[i] = vec.u[rows[i]] / beta;
+  for (int i = threadIdx.x; i < m && i < ns; i += NT) rs[i] = vec.u[rows[i]] / beta;
   for (int c = c0 + threadIdx.x; c < c0 + CT && c < nc; c += NT) {
     vec.x[co + c] = 0.0;
     vec.w[co + c] = 0.0;
@@ -366,7 +372,7 @@ __global__ void __launch_bounds__(NT) lsqr_init_b(fl_blockop op, fl_lsqr_vecs ve
   const double* Bj = op.vals + op.off[j];
   const int64_t ld = op.ld[j];
   for (int c = c0 + wid; c < c0 + CT && c < nc; c += NW) {
-    const double d = col_dot(Bj + c * ld, m, rs, lane);
+    const double d = col_dot(Bj + c * ld, m, rs, lane, ns, vec.u, rows, beta);
     if (lane == 0) {
       vec.vp[co + c] = d;
       ass += d * d;
@@ -439,7 +445,14 @@ int set_smem(const void* fn, size_t bytes) {
   return FL_OK;
 }
 size_t col_smem(const fl_blockop* op) { return (size_t)(op->max_ncols > 0 ? op->max_ncols : 1) * sizeof(double); }
-size_t row_smem(const fl_blockop* op) { return (size_t)(op->max_rows > 0 ? op->max_rows : 1) * sizeof(double); }
+// rows of a block's vector staged in shared memory by the transposed kernels:
+// all of them up to 200 KB, the rest gathered from global memory (col_dot)
+constexpr size_t ROW_STAGE_MAX = 200 * 1024;
+size_t row_smem(const fl_blockop* op) {
+  const size_t b = (size_t)(op->max_rows > 0 ? op->max_rows : 1) * sizeof(double);
+  return b < ROW_STAGE_MAX ? b : ROW_STAGE_MAX;
+}
+int row_staged(const fl_blockop* op) { return (int)(row_smem(op) / sizeof(double)); }
 int grid_rows(const fl_blockop* op) { return (op->nrows + NT - 1) / NT; }
 // one HBM pass per iteration (lsqr_fused.cu) unless a column tile does not fit
 // on chip or FEATLSQ_LSQR=split asks for the two-pass kernels
@@ -468,7 +481,7 @@ extern "C" int fl_blockop_apply_t(const fl_blockop* op, const double* r, double*
   if (op->n_col_tiles == 0) return FL_OK;
   int e = set_smem((const void*)adj_kernel, row_smem(op));
   if (e) return e;
-  adj_kernel<<<op->n_col_tiles, NT, row_smem(op), (cudaStream_t)stream>>>(*op, r, out);
+  adj_kernel<<<op->n_col_tiles, NT, row_smem(op), (cudaStream_t)stream>>>(*op, r, out, row_staged(op));
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
@@ -483,7 +496,7 @@ extern "C" int fl_lsqr_init(const fl_blockop* op, const double* rhs, fl_lsqr_vec
   if (use_fused(op)) return fl::lsqr_fused_init(op, vecs, st, s);
   int e = set_smem((const void*)lsqr_init_b, row_smem(op));
   if (e) return e;
-  lsqr_init_b<<<op->n_col_tiles, NT, row_smem(op), s>>>(*op, *vecs, st);
+  lsqr_init_b<<<op->n_col_tiles, NT, row_smem(op), s>>>(*op, *vecs, st, row_staged(op));
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
@@ -502,7 +515,7 @@ extern "C" int fl_lsqr_iterate_monitored(const fl_blockop* op, fl_lsqr_vecs* vec
     const int64_t it = first_it + k;
     lsqr_qv_kernel<<<op->n_row_tiles, NT, col_smem(op), s>>>(*op, *vecs, st);
     lsqr_ured_kernel<<<grid_rows(op), NT, 0, s>>>(*op, *vecs, st, it);
-    lsqr_qtu_kernel<<<op->n_col_tiles, NT, row_smem(op), s>>>(*op, *vecs, st, it);
+    lsqr_qtu_kernel<<<op->n_col_tiles, NT, row_smem(op), s>>>(*op, *vecs, st, it, row_staged(op));
     if (mon && (e = fl::monitor_step(mon, vecs->x, st, it, s))) return e;
   }
   FL_CHECK_LAUNCH();

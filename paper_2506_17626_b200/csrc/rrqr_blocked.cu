@@ -461,8 +461,10 @@ extern "C" int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t
   if (!(sigma >= 0.0 && sigma < 1.0) || K < NB || K % NB) return FL_ERR_INVALID;
   const int J = A->nblocks;
   if (J == 0) return FL_OK;
-  // shared-memory bounds of K2a (>= 2 staged panel columns) and K2b (F panel)
-  if (A->max_rows > FL_RRQR_BLOCKED_MAX_ROWS || K > FL_RRQR_BLOCKED_MAX_K) return FL_ERR_INVALID;
+  // shared-memory bound of K2b (F panel). Blocks taller than
+  // FL_RRQR_BLOCKED_MAX_ROWS are handled too: their inner panels are factored
+  // in place instead of staged (panel.cu)
+  if (K > FL_RRQR_BLOCKED_MAX_K) return FL_ERR_INVALID;
   Workspace ws = carve(workspace, J, K, store_elems, nullptr);
   // the raw blocks stay intact: the first K2a step reads them and writes the
   // factor copy (same layout, absolute offsets)

@@ -132,4 +132,9 @@ def test_rrqr_route_respects_shared_memory_bounds():
     assert rrqr_route(layout(200, 900)) == "direct"                # K % 32 != 0
     assert rrqr_route(layout(512, 400)) == "direct"                # wide blocks
     assert rrqr_route(layout(BLOCKED_MAX_K + 32, 2000)) == "direct"
-    assert rrqr_route(layout(256, BLOCKED_MAX_ROWS + 16)) == "direct"
+    # no row bound on route R (taller blocks: inner panels factored in place);
+    # narrow blocks go there once the direct kernel's reflector no longer fits
+    assert rrqr_route(layout(256, BLOCKED_MAX_ROWS + 16)) == "blocked"
+    assert rrqr_route(layout(64, 20000)) == "direct"
+    assert rrqr_route(layout(64, 40000)) == "blocked"
+    assert rrqr_route(layout(72, 40000)) == "direct"               # neither route: CapExceededError

@@ -281,13 +281,15 @@ def test_qr_column_pivot_both_routes_match_scipy(fl, K):
     assert np.abs(q @ r - a[:, got.kept]).max() <= 1e-12 * np.abs(a).max()
 
 
-@pytest.mark.parametrize("m,K", [(2500, 128), (4001, 160), (7003, 128), (11770, 192)])
+@pytest.mark.parametrize("m,K", [(2500, 128), (4001, 160), (7003, 128), (11770, 192), (13001, 128),
+                                 (30011, 64)])
 def test_route_r_tall_blocks_match_scipy(fl, m, K):
     """Route R's panel kernel keeps 8, 4 or 2 columns of an inner panel in
-    shared memory depending on the block's rows (<= 2944 / 5888 / 11776);
-    every width, with row counts that are odd or 2 mod 4 (the unaligned
-    starts of the 2-column panels), reproduces LAPACK's factorisation
-    (linalg.py:58-97)."""
+    shared memory depending on the block's rows (<= 2944 / 5888 / 11776) and
+    factors taller blocks in place; every width, with row counts that are odd
+    or 2 mod 4 (the unaligned starts of the 2-column panels), reproduces
+    LAPACK's factorisation (linalg.py:58-97). The last case is a narrow
+    block beyond the direct kernel's on-chip bound."""
     from paper_2506_17626_b200 import _device as D
     from paper_2506_17626_b200.filtering import rrqr_route
     rng = np.random.default_rng(m + K)
@@ -302,6 +304,47 @@ def test_route_r_tall_blocks_match_scipy(fl, m, K):
     q, r = got.q_factor, got.r_factor
     assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-12
     assert np.abs(q @ r - a[:, got.kept]).max() <= 1e-12 * np.abs(a).max()
+
+
+def test_tall_blocks_end_to_end(fl):
+    """Blocks of 40 000 rows (beyond what the panel kernel, the direct RRQR
+    and the transposed product kernels stage on chip): K1, route R with
+    in-place inner panels, the split LSQR kernels with gathered rows, and
+    recovery against the oracle (the reference has no block-size bound)."""
+    from paper_2506_17626_b200 import _device as D, workloads
+    wl = workloads.build("cfg1", S=4, M=128, n=60000, overlap=2.0)
+    sysd = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    assert max(b.rows.size for b in sysd.blocks) > 30000
+    ref = O.assemble(wl.problem, wl.dec, wl.basis, wl.interior_per_dim)
+    for blk, (rows, mat) in zip(sysd.blocks, ref["blocks"]):
+        assert np.array_equal(blk.rows, rows)
+        assert np.abs(blk.matrix - mat).max() <= 1e-13 * np.abs(mat).max()
+    fs = fl.filter_system(sysd, wl.sigma)
+    fb, off = O.filter_system(ref, wl.sigma)
+    assert np.array_equal(fs.kept_columns, np.concatenate([b["kept"] for b in fb]))
+    for blk, ob in zip(fs.blocks, fb):
+        assert np.linalg.norm(blk.r_factor - ob["r"]) <= 1e-10 * np.linalg.norm(ob["r"])
+        q = blk.q_factor
+        assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-12
+    rng = np.random.default_rng(0)
+    M = O.raw_operator(ref)
+    a, r = rng.standard_normal(sysd.column_count), rng.standard_normal(sysd.row_count)
+    assert np.linalg.norm(fl.apply(sysd, a) - M @ a) <= 1e-12 * np.linalg.norm(M @ a)
+    assert np.linalg.norm(fl.apply_transpose(sysd, r) - M.T @ r) <= 1e-12 * np.linalg.norm(M.T @ r)
+    # same operator (the oracle's Q blocks, uploaded): the residual estimates
+    # agree to 1e-9 until the Krylov space of this rank-57 system is
+    # exhausted (iteration ~28; the same happens with 20 000-row blocks,
+    # which fit the staging buffers), and stay within a few percent after
+    oq = D.blocks_from_host(ref["row_count"], [b["rows"] for b in fb], [b["q"] for b in fb])
+    res = fl.lsqr(oq, ref["rhs"], 50)
+    q = O.q_operator(fb, off, ref["row_count"])
+    x50, _, _, _, tr_o = O.lsqr(lambda v: q @ v, lambda u: q.T @ u, q.shape[1], ref["rhs"], 50)
+    got = np.array([rec[1] for rec in res.monitor.records])
+    np.testing.assert_allclose(got[:25], tr_o[:25], rtol=1e-9)
+    np.testing.assert_allclose(got, tr_o, rtol=5e-2)
+    own = fl.lsqr(fl.precondition(fs), sysd.rhs, 50)
+    coeffs = fl.recover_solution(fs, own.solution)
+    assert np.isfinite(coeffs).all() and np.all(coeffs[np.concatenate(fs.dropped_list)] == 0.0)
 
 
 @pytest.mark.parametrize("K", [160, 256])
