@@ -145,6 +145,8 @@ def _solve(fl, blocks, rhs, iters):
     run.init(D.to_dev(rhs))
     run.iterate(1, iters)
     st = run.read_state()
+    tr = D.to_host(run.trace[iters - 1:iters + 1])
+    _solve.last_step = float(abs(tr[0] - tr[1]))  # phi-bar's progress over the last iteration
     return D.to_host(run.x)[:blocks.ncols_total].copy(), float(st.phibar)
 
 
@@ -180,6 +182,7 @@ def test_full_size_solution_within_own_spread(fl, full, golden_dir):
     del ref_ops
     op = fl.precondition(fs)
     y_d, ph_d = _solve(fl, op.device_blocks, sysd.rhs, ITERS)
+    step_d = _solve.last_step
     # D': every entry of A moved by at most 1 ulp (relative 2^-52 noise)
     noise = np.random.default_rng(7)
     pert = fl.assemble(wl.problem, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
@@ -205,8 +208,14 @@ def test_full_size_solution_within_own_spread(fl, full, golden_dir):
     # the spread itself stays small, so the gate above is not vacuous (cfg2,
     # the least well-conditioned after preconditioning, spreads 9.5e-5 in M a)
     assert dp["Ma"] <= 1e-3 and dp["pred"] <= 1e-3
+    # phi-bar: a difference of two scalars against a one-sample scalar spread
+    # can fail by chance (the sample happens to be small), so the gate is the
+    # larger of 10x that spread and one iteration's progress of phi-bar at the
+    # budget (the two runs are then less than one iteration apart)
     sp_ph = abs(ph_p - ph_d)
-    assert abs(ph_d - ph_l) <= max(1e-9 * ph_l, 10.0 * sp_ph)
+    print(f"{name}: |phibar D - L| {abs(ph_d - ph_l):.3e}, 1-ulp spread {sp_ph:.3e}, "
+          f"last iteration's progress {step_d:.3e}")
+    assert abs(ph_d - ph_l) <= max(1e-9 * ph_l, 10.0 * sp_ph, step_d)
     # L1 test error: bounded by the mean prediction change over the spread
     # (|l1(a) - l1(b)| <= mean|a - b| / spread); gated at 10x what the 1-ulp
     # perturbation's prediction change allows
