@@ -282,7 +282,12 @@ def test_qr_column_pivot_both_routes_match_scipy(fl, K):
 
 
 @pytest.mark.parametrize("m,K", [(2500, 128), (4001, 160), (7003, 128), (11770, 192), (13001, 128),
-                                 (30011, 64)])
+                                 (30011, 64),
+                                 # row counts around the leading-dimension padding (16) and the
+                                 # staging thresholds 2944 / 5888 / 11776 of the panel kernel
+                                 (129, 128), (143, 128), (144, 128), (145, 128), (257, 256), (1000, 160),
+                                 (2944, 128), (2945, 128), (5888, 128), (5889, 128), (11776, 128),
+                                 (11777, 128)])
 def test_route_r_tall_blocks_match_scipy(fl, m, K):
     """Route R's panel kernel keeps 8, 4 or 2 columns of an inner panel in
     shared memory depending on the block's rows (<= 2944 / 5888 / 11776) and
