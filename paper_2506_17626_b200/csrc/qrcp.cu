@@ -23,6 +23,11 @@
 // shared counter (68.1 vs 67.6 ms), two 256-thread CTAs per SM (85-90 vs
 // 67.5 ms: DRAM reads 327-351 vs 230 GB, round 2).
 //
+// 256-bit loads in the F-gemv (round 2): 72.9 vs 63.5 ms and 309 vs 235 GB of
+// DRAM reads — LDG.E.ENL2.256 does not keep its lines in L1, so the
+// evict_last reuse across a panel's steps is lost; they are used only in
+// the block update, which streams.
+//
 // The step's critical path is a handful of dependent memory round trips, so
 // the kernel is organised for memory-level parallelism: the column swap is
 // fused with the pivot column's panel update (whose k panel values per row
