@@ -1,11 +1,12 @@
 // K2a panel factorisation: unpivoted Householder QR of one 32-column panel
 // of every block (LAPACK dgeqr2 + dlarft semantics), batched one CTA per
 // block. The panel rows P0..m-1 are factored in inner panels of w columns
-// (w = 8, 4 or 2, the widest whose rows fit in shared memory); each inner
-// panel is factored entirely in shared memory, then applied to the rest of
-// the 32-column panel in compact-WY form as two streaming DMMA passes over
-// those columns (P = V^T X, then X -= V (Tw^T P)) with the loads of four
-// 8-row chunks in flight per warp. Finally the panel's T factor (32 x 32,
+// (w = 8, 4 or 2, the widest whose rows fit in shared memory; blocks too
+// tall for two staged columns are factored in place, 8 columns at a time).
+// Each inner panel is factored on chip, then applied to the rest of the
+// 32-column panel in compact-WY form as two streaming DMMA passes over those
+// columns (P = V^T X, then X -= V (Tw^T P)) with 256-bit accesses, several
+// 16-row chunks in flight per warp. Finally the panel's T factor (32 x 32,
 // upper triangular) is built from the Gram matrix V^T V, streamed the same
 // way (the loaded fragment of an 8-column group is both the A and the B
 // operand of its tiles), and the dlarft recurrence runs on one warp with the
@@ -25,7 +26,7 @@ constexpr int NB = 32;
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
 // (measured on cfg4: 184 KB 2.09 ms per launch, 164 KB 2.14, 132 KB (W = 4) 2.50)
-constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~14 KB static)
+constexpr int SMEM_S = 184 * 1024;  // bytes for the inner-panel columns (+ ~31 KB static)
 // (measured: 256 threads at two CTAs per SM, 84 KB panels, was slower: 2.80 vs 2.25 ms per launch)
 
 // Sum N (a power of two <= 32) per-thread partials across the CTA; results
