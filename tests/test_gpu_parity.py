@@ -311,6 +311,36 @@ def test_route_r_tall_blocks_match_scipy(fl, m, K):
     assert np.abs(q @ r - a[:, got.kept]).max() <= 1e-12 * np.abs(a).max()
 
 
+def test_rhs_evaluated_off_thread(fl):
+    """`assemble` hands the right-hand side (the problem's forcing / lift
+    callables over every point, assembly.py:179-192) to a worker thread; the
+    `rhs` attribute joins on first access, equals the oracle's, and re-raises
+    what a callable raised."""
+    import dataclasses
+    import threading
+    from paper_2506_17626_b200 import workloads
+    wl = workloads.build("cfg1")
+    seen = []
+
+    def forcing(p):
+        seen.append(threading.current_thread().name)
+        return wl.problem.forcing(p)
+    prob = dataclasses.replace(wl.problem, forcing=forcing)
+    sysd = fl.assemble(prob, wl.dec, wl.basis, interior_per_dim=wl.interior_per_dim)
+    ref = O.assemble(wl.problem, wl.dec, wl.basis, wl.interior_per_dim)
+    assert np.array_equal(sysd.rhs, ref["rhs"]) and sysd.rhs is sysd.rhs
+    assert seen == ["featlsq-rhs"]
+
+    def broken(p):
+        raise ValueError("forcing failed")
+    sysd = fl.assemble(dataclasses.replace(wl.problem, forcing=broken), wl.dec, wl.basis,
+                       interior_per_dim=wl.interior_per_dim)
+    fs = fl.filter_system(sysd, wl.sigma)   # the blocks do not depend on the right-hand side
+    assert fs.kept_total > 0
+    with pytest.raises(ValueError, match="forcing failed"):
+        sysd.rhs
+
+
 def test_tall_blocks_end_to_end(fl):
     """Blocks of 40 000 rows (beyond what the panel kernel, the direct RRQR
     and the transposed product kernels stage on chip): K1, route R with
