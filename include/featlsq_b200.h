@@ -158,13 +158,13 @@ int fl_rrqr(const fl_blockop* blocks, int32_t K, int32_t max_rows, double sigma,
  * store_elems = total doubles of the A store. No host synchronisation.
  * Shared-memory bound: K <= FL_RRQR_BLOCKED_MAX_K (else FL_ERR_INVALID); any
  * number of rows (blocks of up to FL_RRQR_BLOCKED_MAX_ROWS rows have the
- * inner panels of K2a staged in shared memory, taller ones are factored in
- * place: slower, same results). fl_rrqr stages one
+ * 8-column inner panels of K2a staged in shared memory, taller ones are
+ * factored in place). fl_rrqr stages one
  * max_rows-long reflector on chip: 8 * (4 K + max_rows) + 4 K bytes <= 220 KB
  * (about 25.8k rows at K = 512), else FL_ERR_INVALID; the host maps blocks
  * that neither route takes to CapExceededError. */
 #define FL_RRQR_BLOCKED_MAX_K 640
-#define FL_RRQR_BLOCKED_MAX_ROWS 11776
+#define FL_RRQR_BLOCKED_MAX_ROWS 2944
 #define FL_RRQR_DIRECT_SMEM_MAX (220 * 1024)
 int64_t fl_rrqr_blocked_workspace(int32_t nblocks, int32_t K, int64_t store_elems);
 int fl_rrqr_blocked(const fl_blockop* A, const fl_blockop* Q, int32_t K, int64_t store_elems,

@@ -1,8 +1,8 @@
 // K2a panel factorisation: unpivoted Householder QR of one 32-column panel
 // of every block (LAPACK dgeqr2 + dlarft semantics), batched one CTA per
-// block. The panel rows P0..m-1 are factored in inner panels of w columns
-// (w = 8, 4 or 2, the widest whose rows fit in shared memory; blocks too
-// tall for two staged columns are factored in place, 8 columns at a time).
+// block. The panel rows P0..m-1 are factored in inner panels of 8 columns,
+// staged in shared memory when their rows fit (<= 2944), else in place in
+// the block.
 // Each inner panel is factored on chip, then applied to the rest of the
 // 32-column panel in compact-WY form as two streaming DMMA passes over those
 // columns (P = V^T X, then X -= V (Tw^T P)) with 256-bit accesses, several
@@ -519,10 +519,12 @@ __global__ void __launch_bounds__(NT, 1) panel_kernel(PanelArgs a) {
   const int M = a.m[j] - a.P0;
   if (M <= 0) return;
   const int cap = SMEM_S / 8;
+  // blocks whose 8-column inner panels do not fit in shared memory (more than
+  // FL_RRQR_BLOCKED_MAX_ROWS rows from this panel on) are factored in place;
+  // measured at cfg5 (4096 to 5832 rows): in place 1.30 ms per launch,
+  // 4-column staged inner panels 1.35
   if (8 * M <= cap) panel_body<8, false>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
-  else if (4 * M <= cap) panel_body<4, false>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
-  else if (2 * M <= cap) panel_body<2, false>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
-  else panel_body<8, true>(a, j, S, red, sc, Tw, Gs, Pw, Zs);  // taller than FL_RRQR_BLOCKED_MAX_ROWS
+  else panel_body<8, true>(a, j, S, red, sc, Tw, Gs, Pw, Zs);
 }
 
 }  // namespace

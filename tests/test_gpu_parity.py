@@ -284,17 +284,16 @@ def test_qr_column_pivot_both_routes_match_scipy(fl, K):
 @pytest.mark.parametrize("m,K", [(2500, 128), (4001, 160), (7003, 128), (11770, 192), (13001, 128),
                                  (30011, 64),
                                  # row counts around the leading-dimension padding (16) and the
-                                 # staging thresholds 2944 / 5888 / 11776 of the panel kernel
+                                 # staging threshold (2944 rows) of the panel kernel
                                  (129, 128), (143, 128), (144, 128), (145, 128), (257, 256), (1000, 160),
                                  (2944, 128), (2945, 128), (5888, 128), (5889, 128), (11776, 128),
                                  (11777, 128)])
 def test_route_r_tall_blocks_match_scipy(fl, m, K):
-    """Route R's panel kernel keeps 8, 4 or 2 columns of an inner panel in
-    shared memory depending on the block's rows (<= 2944 / 5888 / 11776) and
-    factors taller blocks in place; every width, with row counts that are odd
-    or 2 mod 4 (the unaligned starts of the 2-column panels), reproduces
-    LAPACK's factorisation (linalg.py:58-97). The last case is a narrow
-    block beyond the direct kernel's on-chip bound."""
+    """Route R's panel kernel stages its 8-column inner panels in shared
+    memory for blocks of up to 2944 rows and factors taller blocks in place;
+    both, with row counts that are odd, 2 mod 4 or at the thresholds,
+    reproduce LAPACK's factorisation (linalg.py:58-97). (30011, 64) is a
+    narrow block beyond the direct kernel's on-chip bound."""
     from paper_2506_17626_b200 import _device as D
     from paper_2506_17626_b200.filtering import rrqr_route
     rng = np.random.default_rng(m + K)
