@@ -22,6 +22,10 @@ constexpr int RC = 32;            // rows per staged chunk
 // 301.1 ms per two filters); wy<32>, 2 filters: 3 stages 30.3 ms, 2 stages
 // 38.8, 4 stages 42.3.
 constexpr int WY_STAGES64 = 4, WY_STAGES32 = 3;
+// Measured and not kept (round 2): warp-uniform skips of the n-tiles past a
+// tile's last column (the 32-column panel-local updates use half of a 64-column
+// tile): wy<64> 75.3 -> 90.8 ms and wy<32> 30.3 -> 33.2 ms per two filters
+// (the branches around the unrolled MMA loops cost more than the idle tiles).
 template <int NB>
 constexpr int stages_for() { return NB == 64 ? WY_STAGES64 : WY_STAGES32; }
 constexpr int LDS = RC + 4;       // padded column length of a staged chunk
