@@ -53,16 +53,14 @@ __device__ __forceinline__ Jet raw_factor(double t, double mu, double half) {
   return r;
 }
 
-// 1 / d for d in [1, 1e300]: MUFU approximation + two Newton steps (the
-// relative error squares per step: full precision, <= 1 ulp; no special-case
-// branches, which __drcp_rn carries)
+// 1 / d for d in [1, 1e300]: MUFU approximation y0 (relative error e ~ 2^-20)
+// refined as y0 (1 + e + e^2), error e^3: full precision in three FMAs, no
+// special-case branches (which __drcp_rn carries)
 __device__ __forceinline__ double rcp_newton(double d) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  double e = fma(-d, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-d, y, 1.0);
-  return fma(y, e, y);
+  const double e = fma(-d, y, 1.0);
+  return fma(y, fma(e, e, e), y);
 }
 // tanh(x) = em / (em + 2) with em = expm1(2x) in [-1, 1e300]: relative
 // accuracy for small |x| too (1 - 2 / (exp(2x) + 1) loses it to cancellation)
@@ -330,7 +328,7 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
     }
     return tv * c.A + g1 * p1 + g2 * p2;
   };
-  // tanh: g2 = -2 t g1, so entry = t A + g1 (p1 - 2 t p2)
+  // tanh: g2 = -2 t g1, so entry = t A + g1 (p1 + t p2') with p2' = sum_a fp_a^2 (-2 C_a)
   auto entry_tanh = [&](const RowCoef& c, const double (&f1)[MAXD], const double (&f2)[MAXD], double tv) {
     double p1 = f1[0] * c.B[0], p2 = f2[0] * c.C[0];
 #pragma unroll
@@ -339,7 +337,7 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
       p2 += f2[a] * c.C[a];
     }
     const double g1 = fma(-tv, tv, 1.0);
-    return fma(g1, fma(-2.0 * tv, p2, p1), tv * c.A);
+    return fma(g1, fma(tv, p2, p1), tv * c.A);  // c.C holds -2 C on this path (below)
   };
 
   // this thread's table coordinate: q = tid mod tl (axis ta, normalised
@@ -352,6 +350,15 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
     while (ta + 1 < D && tq >= base[ta + 1]) ++ta;
     const int digit = lo[ta] + (tq - base[ta]);
     txa = (d.axes[d.axis_off[ta] + box[2 * ta] + digit] - d.centers[(int64_t)ta * S + sidx[ta]]) * invh[ta];
+  }
+
+  // threads on the tabulated path only use entry_tanh: fold its factor -2
+  // into the rows' C coefficients once (an exact scaling)
+  if (row_tab) {
+#pragma unroll
+    for (int u = 0; u < RPT; ++u)
+#pragma unroll
+      for (int a = 0; a < MAXD; ++a) rc[u].C[a] *= -2.0;
   }
 
   // ---- phase 2: 64-column chunks ----
@@ -370,29 +377,40 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
     }
     if (!store) continue;
     if (row_tab) {
+      // running pointers to the rows' table slots and to the output column
+      // (no index arithmetic per entry)
+      const double* tp[RPT][MAXD];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+#pragma unroll
+        for (int a = 0; a < MAXD; ++a) tp[u][a] = tab + toff[u][a];
+      double* op = out + (int64_t)k0 * ld;
 #pragma unroll 2
-      for (int c = 0; c < nk; ++c) {
+      for (int c = 0; c < nk; ++c, op += ld) {
         const int k = k0 + c;
         double f1[MAXD], f2[MAXD];
         col_terms(k, f1, f2);
+#pragma unroll
+        for (int a = 0; a < D; ++a) asm volatile("" : "+d"(f2[a]));  // shared by the rows, not recomputed per row
         double v[RPT];
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           // expm1 of a sum from the factors' expm1: prod (1 + e_a) - 1
-          double em = tab[c * TLMAX + toff[u][0]];
+          double em = tp[u][0][c * TLMAX];
           if (D > 1) {
-            const double e1 = tab[c * TLMAX + toff[u][1]];
+            const double e1 = tp[u][1][c * TLMAX];
             em = fma(em, e1, em + e1);
           }
           if (D > 2) {
-            const double e2 = tab[c * TLMAX + toff[u][2]];
+            const double e2 = tp[u][2][c * TLMAX];
             em = fma(em, e2, em + e2);
           }
-          v[u] = rc[u].valid ? entry_tanh(rc[u], f1, f2, tanh_from_expm1(em)) : 0.0;
+          // rows past m have all-zero coefficients (row_coef) and read table
+          // slot 0, so their entry is a zero without a per-entry branch
+          v[u] = entry_tanh(rc[u], f1, f2, tanh_from_expm1(em));
         }
 #pragma unroll
-        for (int u = 0; u < RPT; u += 2)
-          *reinterpret_cast<double2*>(out + (int64_t)k * ld + u) = make_double2(v[u], v[u + 1]);
+        for (int u = 0; u < RPT; u += 2) *reinterpret_cast<double2*>(op + u) = make_double2(v[u], v[u + 1]);
       }
     } else {
       for (int c = 0; c < nk; ++c) {
