@@ -53,10 +53,20 @@ __device__ __forceinline__ Jet raw_factor(double t, double mu, double half) {
   return r;
 }
 
-// 1 / d for d in [1, 1e300]: MUFU approximation y0 (relative error e ~ 2^-20)
-// refined as y0 (1 + e + e^2), error e^3: full precision in three FMAs, no
-// special-case branches (which __drcp_rn carries)
+// 1 / d for d in [1, 1e300]: MUFU approximation + two Newton steps (the
+// relative error squares per step: full precision, <= 1 ulp; no special-case
+// branches, which __drcp_rn carries)
 __device__ __forceinline__ double rcp_newton(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+// the tabulated path's form: y0 (1 + e + e^2), e = 1 - d y0 ~ 2^-23, error e^3:
+// one FMA less on the entry's dependent chain
+__device__ __forceinline__ double rcp_newton3(double d) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
   const double e = fma(-d, y, 1.0);
@@ -65,6 +75,7 @@ __device__ __forceinline__ double rcp_newton(double d) {
 // tanh(x) = em / (em + 2) with em = expm1(2x) in [-1, 1e300]: relative
 // accuracy for small |x| too (1 - 2 / (exp(2x) + 1) loses it to cancellation)
 __device__ __forceinline__ double tanh_from_expm1(double em) { return em * rcp_newton(em + 2.0); }
+__device__ __forceinline__ double tanh_from_expm1_tab(double em) { return em * rcp_newton3(em + 2.0); }
 // general argument: expm1(2x) clamped below overflow (tanh is 1.0 in fp64 far before)
 __device__ __forceinline__ double tanh_fast(double x) { return tanh_from_expm1(fmin(expm1(2.0 * x), 1e300)); }
 
@@ -385,7 +396,10 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
 #pragma unroll
         for (int a = 0; a < MAXD; ++a) tp[u][a] = tab + toff[u][a];
       double* op = out + (int64_t)k0 * ld;
-#pragma unroll 2
+      // four columns x two rows = eight independent entry chains per thread
+      // (measured at cfg4, 3 CTAs/SM: unroll 1 / 2 / 4 / 6 / 8 -> 3.48 / 3.39 /
+      // 3.10 / 3.17 / 3.14 ms; 2 CTAs/SM without spills 3.36 / 3.28 at 2 / 4)
+#pragma unroll 4
       for (int c = 0; c < nk; ++c, op += ld) {
         const int k = k0 + c;
         double f1[MAXD], f2[MAXD];
@@ -407,7 +421,7 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
           }
           // rows past m have all-zero coefficients (row_coef) and read table
           // slot 0, so their entry is a zero without a per-entry branch
-          v[u] = entry_tanh(rc[u], f1, f2, tanh_from_expm1(em));
+          v[u] = entry_tanh(rc[u], f1, f2, tanh_from_expm1_tab(em));
         }
 #pragma unroll
         for (int u = 0; u < RPT; u += 2) *reinterpret_cast<double2*>(op + u) = make_double2(v[u], v[u + 1]);
