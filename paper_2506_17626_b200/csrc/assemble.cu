@@ -76,6 +76,32 @@ __device__ __forceinline__ double rcp_newton3(double d) {
 // accuracy for small |x| too (1 - 2 / (exp(2x) + 1) loses it to cancellation)
 __device__ __forceinline__ double tanh_from_expm1(double em) { return em * rcp_newton(em + 2.0); }
 __device__ __forceinline__ double tanh_from_expm1_tab(double em) { return em * rcp_newton3(em + 2.0); }
+// expm1(x) for the table build, |x| <= EXP_SAFE: no special cases and no
+// branches (libm's expm1 diverges within a warp, and every warp of the CTA
+// waits for the slowest at the chunk barrier). x = n ln2 + r, |r| <= ln2 / 2;
+// expm1(x) = 2^n expm1(r) + (2^n - 1), expm1(r) as its degree-13 Taylor
+// polynomial (remainder < 1e-17 relative); relative accuracy near 0 is kept
+// (n = 0: the polynomial itself). A few ulp.
+__device__ __forceinline__ double expm1_table(double x) {
+  const double n = rint(x * 1.4426950408889634);
+  double r = fma(-n, 6.93147180369123816490e-01, x);  // ln2 high part (trailing zeros: n * hi exact)
+  r = fma(-n, 1.90821492927058770002e-10, r);         // ln2 low part
+  double q = 1.6059043836821613e-10;                   // 1/13!
+  q = fma(q, r, 2.08767569878681e-09);                 // 1/12!
+  q = fma(q, r, 2.505210838544172e-08);                // 1/11!
+  q = fma(q, r, 2.755731922398589e-07);                // 1/10!
+  q = fma(q, r, 2.7557319223985893e-06);               // 1/9!
+  q = fma(q, r, 2.48015873015873e-05);                 // 1/8!
+  q = fma(q, r, 1.984126984126984e-04);                // 1/7!
+  q = fma(q, r, 1.388888888888889e-03);                // 1/6!
+  q = fma(q, r, 8.333333333333333e-03);                // 1/5!
+  q = fma(q, r, 4.1666666666666664e-02);               // 1/4!
+  q = fma(q, r, 1.6666666666666666e-01);               // 1/3!
+  q = fma(q, r, 0.5);
+  q = fma(q * r, r, r);                                // expm1(r) = r + r^2 (1/2 + r (1/6 + ...))
+  const double s = __longlong_as_double(((long long)n + 1023LL) << 52);  // 2^n, |n| <= 332
+  return fma(s, q, s - 1.0);
+}
 // general argument: expm1(2x) clamped below overflow (tanh is 1.0 in fp64 far before)
 __device__ __forceinline__ double tanh_fast(double x) { return tanh_from_expm1(fmin(expm1(2.0 * x), 1e300)); }
 
@@ -382,7 +408,7 @@ __global__ void __launch_bounds__(NT, D == 3 ? ASM_MINB - 1 : ASM_MINB) assemble
         for (int c = tc; c < nk; c += tcs) {
           double e = txa * sW[(k0 + c) * D + ta];
           if (ta == 0) e += sB[k0 + c];
-          tab[c * TLMAX + tq] = expm1(2.0 * e);
+          tab[c * TLMAX + tq] = expm1_table(2.0 * e);
         }
       __syncthreads();
     }
